@@ -1,0 +1,170 @@
+/*
+ * hinm_b200.h -- C ABI of the B200-native HiNM hot path (libhinm_b200.so).
+ *
+ * The reference (arXiv 2407.20496, package `hinm`) is pure Python; its hot path
+ * sits behind these functions:
+ *
+ *   hinm_vector_prune   <- hinm.vector_prune(saliency, cfg, sigma_o)       pruning.py:150-164
+ *                          (tile_column_scores :68, _tile_order_and_gains :83,
+ *                           allocate_vector_budget :99, survivors_per_tile :167)
+ *   hinm_nm_select      <- hinm.nm_prune(saliency, vector_mask, cfg, sigma) pruning.py:182-213
+ *                          hinm.encode(weights, masks, sigma, cfg)          pruning.py:284-324
+ *                          (validate_masks :226-254 in mask mode)
+ *   hinm_pack_build     <- (no reference analogue) HiNMEncoding -> tcgen05 operand image
+ *   hinm_compress_bf16  <- `hinm encode --permutation` call chain           cli.py:185-194
+ *   hinm_spmm_bf16      <- hinm.hinm_spmm(enc, X)                           spmm.py:75-99
+ *                          + restore_row_order (out_order=ORIGINAL)        pruning.py:356-360
+ *   hinm_spmm_simt_f32  <- same product on CUDA cores (cross-check kernel, not the product path)
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers owned by the caller; the library never
+ *     allocates or frees caller memory.  bf16 values are passed as uint16_t bit patterns.
+ *   - All work is ordered on `stream` (a cudaStream_t passed as void*).  Functions that
+ *     perform input validation on the device (documented "synchronizing") synchronize the
+ *     stream once at the end to return the validation status; the others are async.
+ *   - Return value: hinm_status_t.  Codes map 1:1 onto the reference's exception classes
+ *     (errors.py:8-49) in the Python wrapper.
+ *   - Layouts: W is m x n row-major with leading dimension ldw (elements).  X is n x B
+ *     channel-major (rows = input channels, tokens contiguous, leading dim ldx).  Y is m x B.
+ */
+#ifndef HINM_B200_H
+#define HINM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HINM_OK = 0,
+  HINM_ERR_SHAPE_MISMATCH = 1, /* ShapeMismatch      */
+  HINM_ERR_INDEX = 2,          /* IndexError         */
+  HINM_ERR_INVARIANT = 3,      /* InvariantViolation */
+  HINM_ERR_GROUPING = 4,       /* GroupingError      */
+  HINM_ERR_BUDGET = 5,         /* BudgetError        */
+  HINM_ERR_DIMENSION = 6,      /* DimensionError     */
+  HINM_ERR_VALUE = 7,          /* ValueError (bad argument / unsupported config) */
+  HINM_ERR_CUDA = 8,           /* CUDA runtime / launch failure */
+  HINM_ERR_WORKSPACE = 9,      /* workspace too small */
+  HINM_ERR_UNSUPPORTED = 10    /* config outside what a kernel implements */
+} hinm_status_t;
+
+/* Output row order of the SpMM epilogue (north-star subsystem 3). */
+enum { HINM_ORDER_SIGMA = 0, HINM_ORDER_ORIGINAL = 1 };
+
+/* Selection source for hinm_nm_select. */
+enum { HINM_SELECT_SCORES = 0, HINM_SELECT_MASK = 1 };
+
+/*
+ * Device pack of one HiNM-encoded matrix.
+ *
+ * Reference view (any V, N:M) -- identical content to hinm.HiNMEncoding:
+ *   tile_ptr[T+1]          prefix sums of k_t (survivors per tile)
+ *   vec_idx[K]             vector_index of every tile, concatenated (sigma_i gather order)
+ *   nm_pos / kept_bf16     tile t occupies V * (k_t/M*N) entries starting at V*tile_ptr[t]/M*N,
+ *                          row-major (V rows x G_t*N): nm_index / kept_values
+ *   sigma_o[m]
+ * SpMM operand image (2:4, V in {32,64,128}; NULL pointers when not built):
+ *   tile_kofs[T+1]         prefix of kp_t = round_up(k_t, 64)
+ *   tile_eofs[T+1]         prefix of ceil(kp_t / 128)  (metadata blocks)
+ *   gidx[kpad_cap]         padded gather index (pad = last real index of the tile)
+ *   a_vals                 compressed A (V x kp_t/2 per tile) in UMMA K-major core-matrix order
+ *   a_meta                 tcgen05 2:4 metadata, V lanes x 16 B per 128-K block
+ */
+typedef struct {
+  int32_t m, n, V, N, M, T;
+  int64_t total_keep;
+  int32_t* tile_ptr;
+  int32_t* vec_idx;
+  uint8_t* nm_pos;
+  uint16_t* kept_bf16;
+  int32_t* sigma_o;
+  int64_t kpad_cap;
+  int64_t meta_words_cap;
+  int32_t* tile_kofs;
+  int32_t* tile_eofs;
+  int32_t* gidx;
+  uint16_t* a_vals;
+  uint32_t* a_meta;
+} hinm_pack_t;
+
+const char* hinm_version(void);
+const char* hinm_status_string(int status);
+
+/* Bytes of device workspace needed by hinm_vector_prune / hinm_compress_bf16. */
+int hinm_compress_workspace(int m, int n, int V, int M, size_t* bytes);
+
+/* Capacities of the SpMM operand image: kpad_cap = K + 64*T, meta words, a_vals elements. */
+int hinm_pack_capacity(int m, int n, int V, int64_t total_keep, int64_t* kpad_cap,
+                       int64_t* meta_words, int64_t* a_vals_elems);
+
+/*
+ * Vector pruning (pruning.py:150-164): column scores of every tile in sigma_o row order
+ * (fp64, numpy summation order), per-tile descending order (ties -> lower column), group
+ * gains, and the global greedy budget (== the total_keep/M smallest keys (-gain, q, t)).
+ * Scores come from `S` (fp64, lds) when non-NULL, else |Wd| (fp64 weights) when non-NULL,
+ * else |W| (bf16, ldw).
+ * Outputs: tile_ptr[T+1] (prefix of k_t), surv[total_keep] ascending survivors per tile
+ * (= the default sigma_i), vector_mask[T*n] (uint8 0/1) when non-NULL.  Async.
+ */
+int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd,
+                      const double* S, int64_t lds, const int32_t* sigma_o, int m, int n, int V, int M, int64_t total_keep,
+                      int32_t* tile_ptr, int32_t* surv, uint8_t* vector_mask,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * N:M selection inside the sigma_i groups of each tile (pruning.py:182-213) and the
+ * reference-view encoding (pruning.py:284-324).  Synchronizing (validates on device):
+ *   - sigma_i[t] must be a permutation of the tile's surviving columns (vector_mask row t)
+ *     -> HINM_ERR_INVARIANT; k_t % M != 0 -> HINM_ERR_GROUPING (first failing tile wins,
+ *     invariant checked before grouping, as in the reference);
+ *   - mode HINM_SELECT_MASK (encode from masks): every (row, group) keeps exactly N and no
+ *     element survives in a pruned vector -> HINM_ERR_INVARIANT (validate_masks :226-254).
+ * Mode SCORES picks the top-N of S (or |W|) per group, ties to the lower position.
+ * In mask mode `total_keep` >= 0 also checks sum(vector_mask) == total_keep (validate_masks :234).
+ * Outputs (any may be NULL): element_mask[m*n] (uint8, original coords; must be zeroed by the
+ * caller), nm_pos / kept_bf16 (from W) / kept_f64 (from Wd) in the reference-view layout above.
+ */
+int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd,
+                   const double* S, int64_t lds, const uint8_t* element_mask_in,
+                   const int32_t* sigma_o, const uint8_t* vector_mask, const int32_t* sig_ptr,
+                   const int32_t* sig_idx, int m, int n, int V, int N, int M, int64_t total_keep,
+                   uint8_t* element_mask_out, uint8_t* nm_pos, uint16_t* kept_bf16,
+                   double* kept_f64, void* stream);
+
+/* Build the SpMM operand image of `pack` from its reference view (2:4, V in {32,64,128}). Async. */
+int hinm_pack_build(hinm_pack_t* pack, void* stream);
+
+/*
+ * Fused compressor (north-star subsystem 1): W bf16 + sigma_o (+ optional sigma_i CSR)
+ * -> complete pack (reference view + operand image).  `pack` buffers are caller-allocated
+ * with the capacities above; sig_ptr/sig_idx NULL selects ascending survivors.
+ * Synchronizing (sigma_i validation).
+ */
+int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t* sigma_o,
+                       const int32_t* sig_ptr, const int32_t* sig_idx, hinm_pack_t* pack,
+                       uint8_t* vector_mask_scratch, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/*
+ * HiNM SpMM on tcgen05 (north-star subsystems 2+3): Y = W_hinm @ X, bf16 in, fp32 accumulate
+ * in TMEM, bf16 out.  Rows of Y in sigma_o order (HINM_ORDER_SIGMA, == hinm_spmm) or original
+ * channel order (HINM_ORDER_ORIGINAL, == restore_row_order(hinm_spmm)).  Requires the operand
+ * image, B % 8 == 0, ldx % 8 == 0, ldy % 8 == 0, 16-byte aligned X/Y.  Async.
+ */
+int hinm_spmm_bf16(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
+                   uint16_t* Y, int64_t ldy, int out_order, void* stream);
+
+/* Same product from the reference view on CUDA cores, fp32 out (test cross-check). Async. */
+int hinm_spmm_simt_f32(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
+                       float* Y, int64_t ldy, int out_order, void* stream);
+
+/* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
+int hinm_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HINM_B200_H */

@@ -1,0 +1,707 @@
+// HiNM compressor on the GPU: vector pruning, N:M selection, reference-view encoding and the
+// tcgen05 operand image.  Bit-exact with the reference (pruning.py) -- every floating-point
+// reduction reproduces numpy's summation order (see common.cuh / oracle/hinm_oracle.py).
+//
+// Kernels:
+//   k_scores      a3  col_score[t,j] = sum_r S[sigma_o[tV+r], j]  (fp64, sigma_o row order)
+//   (cub)         a4  per-tile stable descending sort of scores   (ties -> lower column)
+//   k_gains       a4  gains[t,q] = numpy-pairwise sum of M sorted scores
+//   k_budget      a5  global greedy == G smallest keys (-gain, q, t): threshold select
+//   k_survivors   a6/a7 ascending survivors per tile, vector mask
+//   k_validate_sigma / k_dead_check   a7/a9 invariant checks (pruning.py:196-204, 226-254)
+//   k_nm_select   a8/a10 top-N per sigma_i group, reference view (nm_index, kept_values)
+//   k_pack_*      a10  operand image for the tcgen05 SpMM (padded gather index, UMMA A, E)
+#include <climits>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace hinm {
+
+struct Src {
+  const uint16_t* W;
+  int64_t ldw;
+  const double* Wd;
+  int64_t ldwd;
+  const double* S;
+  int64_t lds;
+  __device__ __forceinline__ double score(int64_t r, int64_t c) const {
+    if (S) return S[r * lds + c];
+    if (Wd) return fabs(Wd[r * ldwd + c]);
+    return bf16_abs_f64(W[r * ldw + c]);
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
+// a3: column scores.  numpy reduces axis 0 of the (V, n) gathered block row by row (sequential)
+// for n >= 2; for n == 1 the operand is contiguous and numpy uses pairwise summation.
+__global__ void k_scores(Src src, const int32_t* __restrict__ sigma_o, int n, int V,
+                         double* __restrict__ scores) {
+  const int t = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t* rows = sigma_o + (int64_t)t * V;
+  double acc;
+  if (n == 1) {
+    auto get = [&](int64_t i) { return src.score(rows[i], 0); };
+    acc = np_pairwise_sum(get, 0, V);
+  } else {
+    acc = src.score(rows[0], j);
+    for (int r = 1; r < V; ++r) acc = acc + src.score(rows[r], j);
+  }
+  scores[(int64_t)t * n + j] = acc + 0.0;  // canonicalise -0.0 (only compared, never emitted)
+}
+
+__global__ void k_iota_cols(int32_t* __restrict__ v, int n, int64_t total) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) v[i] = (int32_t)(i % n);
+}
+
+__global__ void k_segment_offsets(int32_t* __restrict__ off, int T, int n) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= T) off[t] = t * n;
+}
+
+// a4: gains of consecutive M-chunks of the sorted scores (numpy pairwise over the chunk).
+__global__ void k_gains(const double* __restrict__ sorted, int n, int M, int G, int T,
+                        double* __restrict__ gains) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)T * G) return;
+  const int t = (int)(i / G), q = (int)(i % G);
+  const double* base = sorted + (int64_t)t * n + (int64_t)q * M;
+  auto get = [&](int64_t k) { return base[k]; };
+  gains[i] = np_pairwise_sum(get, 0, M) + 0.0;
+}
+
+// Orderable key: ascending key <=> descending gain (gains are >= +0.0 after canonicalisation).
+__device__ __forceinline__ uint64_t gain_key(double g) {
+  return ~(uint64_t)__double_as_longlong(g);
+}
+
+// #{q : key(t,q) <= x} (upper) or < x (lower) for a non-decreasing key row.
+__device__ int row_bound(const double* row, int G, uint64_t x, bool upper) {
+  int lo = 0, hi = G;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    uint64_t k = gain_key(row[mid]);
+    bool go_right = upper ? (k <= x) : (k < x);
+    if (go_right) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int NT>
+__device__ int64_t block_sum64(int64_t v, int64_t* red) {
+  typedef cub::BlockReduce<int64_t, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  int64_t s = BR(tmp).Sum(v);
+  if (threadIdx.x == 0) *red = s;
+  __syncthreads();
+  int64_t out = *red;
+  __syncthreads();
+  return out;
+}
+
+// a5: the greedy allocator of pruning.py:99-129 as a threshold select over the merged key
+// lists.  Single block.  counts_cols[t] = M * (#selected groups of tile t).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_budget(const double* __restrict__ gains, int T, int G,
+                                               int64_t total_groups, int M,
+                                               int32_t* __restrict__ lo_scr,
+                                               int32_t* __restrict__ hi_scr,
+                                               int32_t* __restrict__ tile_ptr) {
+  __shared__ int64_t red;
+  // 1) smallest x with #{key <= x} >= total_groups
+  uint64_t lo = 0, hi = ~0ull;
+  while (lo < hi) {
+    uint64_t mid = lo + ((hi - lo) >> 1);
+    int64_t c = 0;
+    for (int t = threadIdx.x; t < T; t += NT) c += row_bound(gains + (int64_t)t * G, G, mid, true);
+    c = block_sum64<NT>(c, &red);
+    if (c >= total_groups) hi = mid; else lo = mid + 1;
+  }
+  const uint64_t xs = lo;
+  int64_t less = 0;
+  for (int t = threadIdx.x; t < T; t += NT) {
+    const double* row = gains + (int64_t)t * G;
+    int a = row_bound(row, G, xs, false), b = row_bound(row, G, xs, true);
+    lo_scr[t] = a;
+    hi_scr[t] = b;
+    less += a;
+  }
+  __syncthreads();
+  less = block_sum64<NT>(less, &red);
+  const int64_t R = total_groups - less;  // ties at key xs still to take, ordered by (q, t)
+  // 2) smallest Q with F(Q) = sum_t clamp(min(hi, Q+1) - lo, 0) >= R
+  int qlo = 0, qhi = G;  // Q in [0, G)
+  if (R > 0) {
+    qhi = G - 1;
+    while (qlo < qhi) {
+      int mid = (qlo + qhi) >> 1;
+      int64_t f = 0;
+      for (int t = threadIdx.x; t < T; t += NT) {
+        int v = min(hi_scr[t], mid + 1) - lo_scr[t];
+        f += v > 0 ? v : 0;
+      }
+      f = block_sum64<NT>(f, &red);
+      if (f >= R) qhi = mid; else qlo = mid + 1;
+    }
+  }
+  const int Q = qlo;
+  int64_t below = 0;
+  if (R > 0) {
+    for (int t = threadIdx.x; t < T; t += NT) {
+      int v = min(hi_scr[t], Q) - lo_scr[t];
+      below += v > 0 ? v : 0;
+    }
+    below = block_sum64<NT>(below, &red);
+  }
+  int64_t rem = R - below;  // tiles (in t order) with lo <= Q < hi that take one more
+  // 3) counts + exclusive prefix over tiles (chunked block scan)
+  typedef cub::BlockScan<int64_t, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ int64_t carry_at, carry_ptr;
+  if (threadIdx.x == 0) { carry_at = 0; carry_ptr = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += NT) {
+    int t = base + threadIdx.x;
+    int64_t at_q = 0, cnt = 0;
+    if (t < T) {
+      int l = lo_scr[t], h = hi_scr[t];
+      if (R > 0) {
+        int v = min(h, Q) - l;
+        cnt = l + (v > 0 ? v : 0);
+        at_q = (l <= Q && Q < h) ? 1 : 0;
+      } else {
+        cnt = l;
+      }
+    }
+    int64_t excl_at;
+    BS(scan_tmp).ExclusiveSum(at_q, excl_at);
+    __syncthreads();
+    if (at_q && carry_at + excl_at < rem) cnt += 1;
+    int64_t cols = cnt * M, excl_cols;
+    BS(scan_tmp).ExclusiveSum(cols, excl_cols);
+    __syncthreads();
+    if (t < T) tile_ptr[t] = (int32_t)(carry_ptr + excl_cols);
+    // chunk totals
+    int64_t tot_at = block_sum64<NT>(at_q, &red);
+    int64_t tot_cols = block_sum64<NT>(cols, &red);
+    if (threadIdx.x == 0) { carry_at += tot_at; carry_ptr += tot_cols; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
+}
+
+// a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_survivors(const int32_t* __restrict__ order, int n,
+                                                  const int32_t* __restrict__ tile_ptr,
+                                                  int32_t* __restrict__ surv,
+                                                  uint8_t* __restrict__ vmask) {
+  extern __shared__ uint8_t flags[];
+  const int t = blockIdx.x;
+  const int k = tile_ptr[t + 1] - tile_ptr[t];
+  for (int j = threadIdx.x; j < n; j += NT) flags[j] = 0;
+  __syncthreads();
+  const int32_t* ord = order + (int64_t)t * n;
+  for (int i = threadIdx.x; i < k; i += NT) flags[ord[i]] = 1;
+  __syncthreads();
+  if (vmask)
+    for (int j = threadIdx.x; j < n; j += NT) vmask[(int64_t)t * n + j] = flags[j];
+  typedef cub::BlockScan<int, NT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  int32_t* out = surv + tile_ptr[t];
+  for (int base = 0; base < n; base += NT) {
+    int j = base + threadIdx.x;
+    int f = (j < n) ? flags[j] : 0, ex, tot;
+    BS(tmp).ExclusiveSum(f, ex, tot);
+    if (f) out[carry + ex] = j;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// Error ranks (per tile, lowest (tile, rank) reported): the reference's check order.
+enum : int {
+  RANK_TOTAL = 0,        // validate_masks: sum(vm) != total_keep (before any tile)
+  RANK_SIGMA_SET = 1,    // sigma_i[t] != survivors (InvariantViolation)
+  RANK_GROUPING = 2,     // k_t % M != 0 (GroupingError in nm_prune, Invariant in encode)
+  RANK_DEAD = 3,         // element kept inside a pruned vector
+  RANK_GROUP_COUNT = 4,  // a group keeps != N elements
+};
+
+// a7/a9: sigma_i[t] must be a permutation of the survivors of vector_mask row t.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_validate_sigma(const uint8_t* __restrict__ vmask, int n,
+                                                       const int32_t* __restrict__ sig_ptr,
+                                                       const int32_t* __restrict__ sig_idx, int M,
+                                                       int mask_mode, int* __restrict__ err,
+                                                       unsigned long long* __restrict__ vm_total) {
+  extern __shared__ uint32_t bits[];  // seen-bitmap
+  const int t = blockIdx.x;
+  const int words = (n + 31) / 32;
+  for (int w = threadIdx.x; w < words; w += NT) bits[w] = 0u;
+  __syncthreads();
+  const uint8_t* row = vmask + (int64_t)t * n;
+  int surv = 0;
+  for (int j = threadIdx.x; j < n; j += NT) surv += row[j] ? 1 : 0;
+  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b;
+  bool bad = false;
+  for (int i = threadIdx.x; i < k; i += NT) {
+    int j = sig_idx[b + i];
+    if (j < 0 || j >= n || !row[j]) { bad = true; continue; }
+    uint32_t old = atomicOr(&bits[j >> 5], 1u << (j & 31));
+    if (old & (1u << (j & 31))) bad = true;  // repeated column
+  }
+  typedef cub::BlockReduce<int, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  int tot = BR(tmp).Sum(surv);
+  __syncthreads();
+  int anybad = BR(tmp).Sum(bad ? 1 : 0);
+  if (threadIdx.x == 0) {
+    if (vm_total) atomicAdd(vm_total, (unsigned long long)tot);
+    if (mask_mode) {
+      // validate_masks order: survivor count % M, then sigma set
+      if (tot % M != 0) report_error(err, t, RANK_GROUPING);
+      else if (anybad || tot != k) report_error(err, t, RANK_SIGMA_SET);
+    } else {
+      if (anybad || tot != k) report_error(err, t, RANK_SIGMA_SET);
+      else if (k % M != 0) report_error(err, t, RANK_GROUPING);
+    }
+  }
+}
+
+// a9: no element of tile t's rows may be kept in a column pruned for that tile.
+__global__ void k_dead_check(const uint8_t* __restrict__ em, const uint8_t* __restrict__ vmask,
+                             const int32_t* __restrict__ sigma_o, int n, int V,
+                             int* __restrict__ err) {
+  const int p = blockIdx.y;  // permuted row position
+  const int t = p / V;
+  const int row = sigma_o[p];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    if (em[(int64_t)row * n + j] && !vmask[(int64_t)t * n + j]) report_error(err, t, RANK_DEAD);
+}
+
+// Tile owning global group g: largest t with tile_ptr[t] / M <= g.
+__device__ __forceinline__ int tile_of_group(const int32_t* __restrict__ tile_ptr, int T, int M,
+                                             int64_t g) {
+  int lo = 0, hi = T;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (tile_ptr[mid] / M <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// a8/a10: one thread per (group, row).  SCORES mode: top-N of the group by saliency, ties to
+// the lower in-group position (stable argsort of -S).  MASK mode: the positions the element
+// mask keeps (must be exactly N).  Positions are emitted ascending (nm_index).
+__global__ void k_nm_select(int mode, Src src, const uint8_t* __restrict__ em_in,
+                            const int32_t* __restrict__ sigma_o,
+                            const int32_t* __restrict__ sig_ptr,
+                            const int32_t* __restrict__ sig_idx, int n, int V, int N, int M,
+                            int T, int64_t total_groups, uint8_t* __restrict__ em_out,
+                            uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept_bf16,
+                            double* __restrict__ kept_f64, int* __restrict__ err) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total_groups * V) return;
+  const int64_t g = gid / V;  // global group index
+  const int r = (int)(gid % V);
+  const int t = tile_of_group(sig_ptr, T, M, g);
+  const int64_t g_in = g - sig_ptr[t] / M;
+  const int Gt = (sig_ptr[t + 1] - sig_ptr[t]) / M;
+  const int32_t* cols = sig_idx + sig_ptr[t] + g_in * M;
+  const int64_t row = sigma_o[(int64_t)t * V + r];
+  int pos[16];
+  int npos = 0;
+  if (mode == HINM_SELECT_SCORES) {
+    double s[32];
+    for (int i = 0; i < M; ++i) s[i] = src.score(row, cols[i]);
+    for (int i = 0; i < M; ++i) {
+      int rank = 0;
+      for (int k = 0; k < M; ++k) rank += (s[k] > s[i]) || (s[k] == s[i] && k < i);
+      if (rank < N) pos[npos++] = i;  // ascending by construction
+    }
+  } else {
+    for (int i = 0; i < M; ++i)
+      if (em_in[row * n + cols[i]]) {
+        if (npos < 16) pos[npos] = i;
+        ++npos;
+      }
+    if (npos != N) {
+      report_error(err, t, RANK_GROUP_COUNT);
+      return;
+    }
+  }
+  const int64_t base = (int64_t)V * (sig_ptr[t] / M) * N + (int64_t)r * Gt * N + g_in * N;
+  for (int s2 = 0; s2 < N; ++s2) {
+    const int p = pos[s2];
+    const int64_t col = cols[p];
+    if (nm_pos) nm_pos[base + s2] = (uint8_t)p;
+    if (kept_bf16 && src.W) kept_bf16[base + s2] = src.W[row * src.ldw + col];
+    if (kept_f64 && src.Wd) kept_f64[base + s2] = src.Wd[row * src.ldwd + col];
+    if (em_out) em_out[row * n + col] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Operand image for the tcgen05 SpMM (see spmm_sm100.cu for the consumer side).
+//   kp_t = round_up(k_t, 64); a stage covers 64 logical K = 32 compressed values per row.
+//   a_vals, per tile / 64-block / MMA-step (32 logical K): V rows x 16 compressed bf16 in the
+//   UMMA K-major SWIZZLE_NONE canonical layout: 8x(16 B) core matrices, LBO = 128 B (K),
+//   SBO = 256 B (8-row groups).
+//   a_meta, per tile / 128-K block: V TMEM lanes x 4 words (word w = MMA step w of the block).
+//   Row m = m0 + 8*m1 + 16*m2 at K-half k1 lives in lane m0 + 8*k1 + 16*m2, bits 16*m1 + 4*c,
+//   nibble = p0 | p1 << 2 (cute TensorEAtom_MMA_F16 / tmem_e_frg, flashinfer-vendored CUTLASS).
+__global__ void k_pack_offsets(const int32_t* __restrict__ tile_ptr, int T,
+                               int32_t* __restrict__ kofs, int32_t* __restrict__ eofs) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t ka = 0, ea = 0;
+  for (int t = 0; t < T; ++t) {
+    kofs[t] = ka;
+    eofs[t] = ea;
+    int k = tile_ptr[t + 1] - tile_ptr[t];
+    int kp = (int)round_up(k, 64);
+    ka += kp;
+    ea += (int)ceil_div(kp, 128);
+  }
+  kofs[T] = ka;
+  eofs[T] = ea;
+}
+
+__device__ __forceinline__ int64_t aval_offset(int64_t kofs_t, int V, int r, int kc) {
+  const int b = kc >> 5, kcb = kc & 31, j = kcb >> 4, kcs = kcb & 15;
+  return (kofs_t >> 1) * V + (int64_t)b * 32 * V + (int64_t)j * 16 * V + (r >> 3) * 128 +
+         (kcs >> 3) * 64 + (r & 7) * 8 + (kcs & 7);
+}
+
+__global__ void k_pack_vals(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ kofs,
+                            const uint16_t* __restrict__ kept, int V, int T, int64_t total_groups,
+                            uint16_t* __restrict__ a_vals) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total_groups * V) return;
+  const int64_t g = gid / V;
+  const int r = (int)(gid % V);
+  const int t = tile_of_group(tile_ptr, T, 4, g);
+  const int64_t g_in = g - tile_ptr[t] / 4;
+  const int Gt = (tile_ptr[t + 1] - tile_ptr[t]) / 4;
+  const int64_t src = (int64_t)V * (tile_ptr[t] / 4) * 2 + (int64_t)r * Gt * 2 + g_in * 2;
+  const int64_t ko = kofs[t];
+  a_vals[aval_offset(ko, V, r, (int)(2 * g_in))] = kept[src];
+  a_vals[aval_offset(ko, V, r, (int)(2 * g_in + 1))] = kept[src + 1];
+}
+
+// One thread per (tile, 128-block, lane, word): composes the 8 nibbles of the word.
+__global__ void k_pack_meta(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ eofs,
+                            const uint8_t* __restrict__ nm_pos, int V, int T,
+                            uint32_t* __restrict__ a_meta) {
+  const int t = blockIdx.y;
+  const int nblk = eofs[t + 1] - eofs[t];
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nblk * V * 4) return;
+  const int w = (int)(idx & 3);
+  const int lane = (int)((idx >> 2) % V);
+  const int eb = (int)((idx >> 2) / V);
+  const int Gt = (tile_ptr[t + 1] - tile_ptr[t]) / 4;
+  const int64_t base = (int64_t)V * (tile_ptr[t] / 4) * 2;
+  const int m0 = lane & 7, k1 = (lane >> 3) & 1, m2 = lane >> 4;
+  uint32_t word = 0;
+#pragma unroll
+  for (int m1 = 0; m1 < 2; ++m1) {
+    const int r = m0 + 8 * m1 + 16 * m2;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int g = 32 * eb + 8 * w + 4 * k1 + c;  // 2:4 group (chunk) index in the tile
+      uint32_t nib = 0x4u;                         // padding: positions {0,1}, values zero
+      if (r < V && g < Gt) {
+        const uint8_t* p = nm_pos + base + (int64_t)r * Gt * 2 + (int64_t)g * 2;
+        nib = (uint32_t)p[0] | ((uint32_t)p[1] << 2);
+      }
+      word |= nib << (16 * m1 + 4 * c);
+    }
+  }
+  a_meta[((int64_t)eofs[t] + eb) * V * 4 + (int64_t)lane * 4 + w] = word;
+}
+
+__global__ void k_pack_gidx(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ kofs,
+                            const int32_t* __restrict__ vec_idx, int32_t* __restrict__ gidx) {
+  const int t = blockIdx.y;
+  const int k = tile_ptr[t + 1] - tile_ptr[t];
+  const int kp = kofs[t + 1] - kofs[t];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kp; i += gridDim.x * blockDim.x) {
+    int v = (i < k) ? vec_idx[tile_ptr[t] + i] : (k > 0 ? vec_idx[tile_ptr[t] + k - 1] : 0);
+    gidx[kofs[t] + i] = v;
+  }
+}
+
+}  // namespace hinm
+
+// ---------------------------------------------------------------------------------------------
+// Host entry points (C ABI, include/hinm_b200.h)
+// ---------------------------------------------------------------------------------------------
+namespace hinm {
+namespace {
+
+struct WsLayout {
+  size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, err, cub, total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int cub_sort_bytes(int T, int n, size_t* bytes) {
+  size_t b = 0;
+  int64_t items = (int64_t)T * n;
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+      nullptr, b, (const double*)nullptr, (double*)nullptr, (const int32_t*)nullptr,
+      (int32_t*)nullptr, items, T, (const int32_t*)nullptr, (const int32_t*)nullptr + 1, 0, 64,
+      (cudaStream_t)0);
+  if (e != cudaSuccess) return HINM_ERR_CUDA;
+  *bytes = b;
+  return HINM_OK;
+}
+
+int ws_layout(int m, int n, int V, int M, WsLayout* L) {
+  if (V < 1 || M < 1 || m < 1 || n < 1 || m % V) return HINM_ERR_DIMENSION;
+  const int64_t T = m / V, G = n / M, Tn = T * n;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  L->scores = take(8 * Tn);
+  L->sorted = take(8 * Tn);
+  L->vals_in = take(4 * Tn);
+  L->order = take(4 * Tn);
+  L->offsets = take(4 * (T + 1));
+  L->gains = take(8 * T * (G > 0 ? G : 1));
+  L->lo = take(4 * T);
+  L->hi = take(4 * T);
+  L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
+  L->err = take(16);
+  size_t cb = 0;
+  int st = cub_sort_bytes((int)T, n, &cb);
+  if (st) return st;
+  L->cub = take(cb);
+  L->total = off;
+  return HINM_OK;
+}
+
+int status_from_rank(int code, int mask_mode) {
+  if (code == INT_MAX) return HINM_OK;
+  int rank = code % 16;
+  if (rank == RANK_GROUPING && !mask_mode) return HINM_ERR_GROUPING;
+  return HINM_ERR_INVARIANT;
+}
+
+}  // namespace
+}  // namespace hinm
+
+using namespace hinm;
+
+extern "C" int hinm_compress_workspace(int m, int n, int V, int M, size_t* bytes) {
+  WsLayout L;
+  int st = ws_layout(m, n, V, M, &L);
+  if (st) return st;
+  *bytes = L.total;
+  return HINM_OK;
+}
+
+extern "C" int hinm_pack_capacity(int m, int n, int V, int64_t total_keep, int64_t* kpad_cap,
+                                  int64_t* meta_words, int64_t* a_vals_elems) {
+  if (V < 1 || m % V) return HINM_ERR_DIMENSION;
+  const int64_t T = m / V;
+  const int64_t kp = total_keep + 64 * T;
+  if (kpad_cap) *kpad_cap = kp;
+  if (meta_words) *meta_words = (kp / 128 + T) * V * 4;
+  if (a_vals_elems) *a_vals_elems = (int64_t)V * kp / 2;
+  (void)n;
+  return HINM_OK;
+}
+
+extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd,
+                                 const double* S, int64_t lds, const int32_t* sigma_o, int m,
+                                 int n, int V, int M, int64_t total_keep, int32_t* tile_ptr,
+                                 int32_t* surv, uint8_t* vector_mask, void* workspace,
+                                 size_t workspace_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!W && !Wd && !S) return HINM_ERR_VALUE;
+  WsLayout L;
+  int st = ws_layout(m, n, V, M, &L);
+  if (st) return st;
+  if (!workspace || workspace_bytes < L.total) return HINM_ERR_WORKSPACE;
+  const int T = m / V, G = n / M;
+  if (total_keep % M != 0) return HINM_ERR_BUDGET;
+  const int64_t groups = total_keep / M;
+  if (groups > (int64_t)T * G) return HINM_ERR_BUDGET;
+  if (n > 200 * 1024) return HINM_ERR_UNSUPPORTED;
+  char* ws = (char*)workspace;
+  double* scores = (double*)(ws + L.scores);
+  double* sorted = (double*)(ws + L.sorted);
+  int32_t* vals_in = (int32_t*)(ws + L.vals_in);
+  int32_t* order = (int32_t*)(ws + L.order);
+  int32_t* offsets = (int32_t*)(ws + L.offsets);
+  double* gains = (double*)(ws + L.gains);
+  Src src{W, ldw, Wd, ldwd, S, lds};
+
+  k_scores<<<dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream>>>(src, sigma_o, n, V, scores);
+  HINM_LAUNCH_CHECK();
+  const int64_t Tn = (int64_t)T * n;
+  k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
+  k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
+  HINM_LAUNCH_CHECK();
+  size_t cb = workspace_bytes - L.cub;
+  HINM_CUDA_TRY(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+      ws + L.cub, cb, scores, sorted, vals_in, order, Tn, T, offsets, offsets + 1, 0, 64, stream));
+  if (G > 0) {
+    k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains);
+    HINM_LAUNCH_CHECK();
+  }
+  k_budget<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, (int32_t*)(ws + L.lo),
+                                         (int32_t*)(ws + L.hi), tile_ptr);
+  HINM_LAUNCH_CHECK();
+  const size_t smem = (size_t)n;
+  if (smem > 48 * 1024)
+    HINM_CUDA_TRY(cudaFuncSetAttribute(k_survivors<1024>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_survivors<1024><<<T, 1024, smem, stream>>>(order, n, tile_ptr, surv, vector_mask);
+  HINM_LAUNCH_CHECK();
+  return HINM_OK;
+}
+
+extern "C" int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const double* Wd,
+                              int64_t ldwd, const double* S, int64_t lds,
+                              const uint8_t* element_mask_in, const int32_t* sigma_o,
+                              const uint8_t* vector_mask, const int32_t* sig_ptr,
+                              const int32_t* sig_idx, int m, int n, int V, int N, int M,
+                              int64_t total_keep, uint8_t* element_mask_out, uint8_t* nm_pos,
+                              uint16_t* kept_bf16, double* kept_f64, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (V < 1 || m % V) return HINM_ERR_DIMENSION;
+  if (M > 32 || N > 16 || N < 1 || N > M) return HINM_ERR_UNSUPPORTED;
+  if (mode == HINM_SELECT_SCORES && !W && !Wd && !S) return HINM_ERR_VALUE;
+  if (mode == HINM_SELECT_MASK && !element_mask_in) return HINM_ERR_VALUE;
+  const int T = m / V;
+  const int mask_mode = mode == HINM_SELECT_MASK;
+  int* d_err = nullptr;
+  HINM_CUDA_TRY(cudaMallocAsync((void**)&d_err, 64, stream));
+  unsigned long long* d_tot = (unsigned long long*)(d_err + 4);
+  int h_err[4] = {INT_MAX, 0, 0, 0};
+  unsigned long long h_tot = 0;
+  int32_t K = 0;
+  int status = HINM_OK;
+  auto fetch = [&]() -> int {
+    HINM_CUDA_TRY(cudaMemcpyAsync(h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, stream));
+    HINM_CUDA_TRY(cudaMemcpyAsync(&h_tot, d_tot, 8, cudaMemcpyDeviceToHost, stream));
+    HINM_CUDA_TRY(cudaStreamSynchronize(stream));
+    return HINM_OK;
+  };
+  const int init = INT_MAX;
+  const size_t vsmem = ((size_t)n + 31) / 32 * 4;
+  if (cudaMemcpyAsync(d_err, &init, sizeof(int), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaMemsetAsync(d_tot, 0, 8, stream) != cudaSuccess) {
+    status = HINM_ERR_CUDA;
+    goto done;
+  }
+  if (vsmem > 48 * 1024 &&
+      cudaFuncSetAttribute(k_validate_sigma<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)vsmem) != cudaSuccess) {
+    status = HINM_ERR_CUDA;
+    goto done;
+  }
+  k_validate_sigma<256><<<T, 256, vsmem, stream>>>(vector_mask, n, sig_ptr, sig_idx, M, mask_mode,
+                                                   d_err, d_tot);
+  if (cudaGetLastError() != cudaSuccess || fetch()) { status = HINM_ERR_CUDA; goto done; }
+  if (mask_mode && total_keep >= 0 && (int64_t)h_tot != total_keep) {
+    status = HINM_ERR_INVARIANT;
+    goto done;
+  }
+  if ((status = status_from_rank(h_err[0], mask_mode))) goto done;
+  if (mask_mode) {
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(n, 256), 64), m);
+    k_dead_check<<<grid, 256, 0, stream>>>(element_mask_in, vector_mask, sigma_o, n, V, d_err);
+    if (cudaGetLastError() != cudaSuccess || fetch()) { status = HINM_ERR_CUDA; goto done; }
+    if ((status = status_from_rank(h_err[0], 1))) goto done;
+  }
+  if (cudaMemcpyAsync(&K, sig_ptr + T, 4, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess) {
+    status = HINM_ERR_CUDA;
+    goto done;
+  }
+  if (K / M > 0) {
+    const int64_t groups = K / M;
+    Src src{W, ldw, Wd, ldwd, S, lds};
+    k_nm_select<<<(unsigned)ceil_div(groups * V, 256), 256, 0, stream>>>(
+        mode, src, element_mask_in, sigma_o, sig_ptr, sig_idx, n, V, N, M, T, groups,
+        element_mask_out, nm_pos, kept_bf16, kept_f64, d_err);
+    if (cudaGetLastError() != cudaSuccess) { status = HINM_ERR_CUDA; goto done; }
+  }
+  if (fetch()) { status = HINM_ERR_CUDA; goto done; }
+  status = status_from_rank(h_err[0], 1);
+done:
+  cudaFreeAsync(d_err, stream);
+  return status;
+}
+
+extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!p) return HINM_ERR_VALUE;
+  if (p->N != 2 || p->M != 4) return HINM_ERR_UNSUPPORTED;
+  if (p->V != 32 && p->V != 64 && p->V != 128) return HINM_ERR_UNSUPPORTED;
+  if (!p->tile_kofs || !p->tile_eofs || !p->gidx || !p->a_vals || !p->a_meta) return HINM_ERR_VALUE;
+  const int T = p->T, V = p->V;
+  int64_t kcap = 0, mcap = 0, acap = 0;
+  hinm_pack_capacity(p->m, p->n, V, p->total_keep, &kcap, &mcap, &acap);
+  if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
+  k_pack_offsets<<<1, 32, 0, stream>>>(p->tile_ptr, T, p->tile_kofs, p->tile_eofs);
+  HINM_LAUNCH_CHECK();
+  HINM_CUDA_TRY(cudaMemsetAsync(p->a_vals, 0, (size_t)acap * 2, stream));
+  const int64_t groups = p->total_keep / 4;
+  if (groups > 0) {
+    k_pack_vals<<<(unsigned)ceil_div(groups * V, 256), 256, 0, stream>>>(
+        p->tile_ptr, p->tile_kofs, p->kept_bf16, V, T, groups, p->a_vals);
+    HINM_LAUNCH_CHECK();
+  }
+  // a tile has at most ceil(round_up(n, 64) / 128) metadata blocks
+  const int64_t max_blocks = ceil_div(round_up(p->n, 64), 128);
+  dim3 gm((unsigned)ceil_div(max_blocks * V * 4, 256), T);
+  k_pack_meta<<<gm, 256, 0, stream>>>(p->tile_ptr, p->tile_eofs, p->nm_pos, V, T, p->a_meta);
+  HINM_LAUNCH_CHECK();
+  dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p->n, 256), 64)), T);
+  k_pack_gidx<<<gg, 256, 0, stream>>>(p->tile_ptr, p->tile_kofs, p->vec_idx, p->gidx);
+  HINM_LAUNCH_CHECK();
+  return HINM_OK;
+}
+
+extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t* sigma_o,
+                                  const int32_t* sig_ptr, const int32_t* sig_idx, hinm_pack_t* p,
+                                  uint8_t* vmask, void* workspace, size_t workspace_bytes,
+                                  void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!p || !W || !sigma_o || !vmask) return HINM_ERR_VALUE;
+  WsLayout L;
+  int st = ws_layout(p->m, p->n, p->V, p->M, &L);
+  if (st) return st;
+  if (!workspace || workspace_bytes < L.total) return HINM_ERR_WORKSPACE;
+  const bool own_sigma = sig_idx == nullptr;
+  int32_t* surv = own_sigma ? p->vec_idx : (int32_t*)((char*)workspace + L.surv_tmp);
+  int32_t* tptr = p->tile_ptr;
+  st = hinm_vector_prune(W, ldw, nullptr, 0, nullptr, 0, sigma_o, p->m, p->n, p->V, p->M,
+                         p->total_keep, tptr, surv, vmask, workspace, workspace_bytes, stream_);
+  if (st) return st;
+  const int32_t* sp = own_sigma ? tptr : sig_ptr;
+  const int32_t* si = own_sigma ? surv : sig_idx;
+  st = hinm_nm_select(HINM_SELECT_SCORES, W, ldw, nullptr, 0, nullptr, 0, nullptr, sigma_o, vmask,
+                      sp, si, p->m, p->n, p->V, p->N, p->M, -1, nullptr, p->nm_pos, p->kept_bf16,
+                      nullptr, stream_);
+  if (st) return st;
+  if (!own_sigma)
+    HINM_CUDA_TRY(cudaMemcpyAsync(p->vec_idx, sig_idx, (size_t)p->total_keep * 4,
+                                  cudaMemcpyDeviceToDevice, stream));
+  if (p->sigma_o != sigma_o)
+    HINM_CUDA_TRY(cudaMemcpyAsync(p->sigma_o, sigma_o, (size_t)p->m * 4, cudaMemcpyDeviceToDevice,
+                                  stream));
+  if (p->a_vals) return hinm_pack_build(p, stream_);
+  return HINM_OK;
+}

@@ -1,0 +1,449 @@
+// HiNM SpMM on Blackwell (sm_100a): TMA gather4 of the kept activation rows + 2:4 sparse
+// tcgen05.mma.sp into TMEM + fused sigma_o row-scatter epilogue.
+//
+//   Y[sigma_o[tV + r], b] = sum_k A_t[r, k] * X[gidx_t[k], b]      (spmm.py:88-98 + pruning.py:356)
+//
+// Work unit = (tile t, block of BN=256 tokens).  Persistent grid (one CTA per SM), units
+// distributed round-robin in token-block-major order so the X token block stays L2 resident
+// while every tile consumes it.
+//
+// Warp roles (192 threads):
+//   warp 0      producer: per 64-K stage, one bulk copy of the compressed A block (V x 64 B),
+//               one bulk copy of the 2:4 metadata every other stage (V x 16 B for 128 K), and
+//               64 TMA gather4 (16 lanes x 4 token sub-blocks) of X rows -> SWIZZLE_128B
+//               MN-major B operand (64 K-rows x 256 tokens)
+//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.cp of the metadata into a
+//               TMEM ring, 2 x tcgen05.mma.sp (M=128, N=256, K=32) per stage, tcgen05.commit
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> bf16 -> 16 B stores to row sigma_o[tV+r]
+//
+// V = 64 (and 32) use the M=128 instruction with rows >= V ignored: the A descriptor's upper
+// row groups alias neighbouring smem and those accumulator lanes are never read.  The M=128
+// and M=64 instructions cost the same tensor-pipe cycles (B300_MICROARCH.md: floor =
+// max(M,128)*N/256), so this costs smem read bandwidth only.
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace hinm {
+namespace sm100 {
+
+constexpr int BN = 256;                        // tokens per unit (UMMA N)
+constexpr int BK = 64;                         // logical K per pipeline stage
+constexpr int STAGES = 5;
+constexpr int NUM_THREADS = 192;
+constexpr int B_STAGE = BK * BN * 2;           // 32 KB of gathered X per stage
+constexpr int E_STAGE = 128 * 16;              // 128 lanes x 16 B metadata image per stage slot
+constexpr int TMEM_COLS = 512;
+constexpr int E_COL = 256;                     // metadata ring after the 256-column accumulator
+constexpr int E_SLOTS = 4;
+constexpr uint32_t META_PAD = 0x44444444u;     // 2:4 nibble {0,1} for rows >= V
+
+struct Params {
+  const int32_t* tile_kofs;
+  const int32_t* tile_eofs;
+  const int32_t* gidx;
+  const uint16_t* a_vals;
+  const uint32_t* a_meta;
+  const int32_t* sigma_o;
+  uint16_t* Y;
+  int64_t ldy;
+  int B;
+  int T;
+  int V;
+  int units;
+  int out_order;
+};
+
+struct SmemLayout {
+  uint32_t a, e, bar, tmem, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int V) {
+  SmemLayout L;
+  L.a = STAGES * B_STAGE;
+  L.e = L.a + STAGES * V * 64 + 4096;          // 4 KB slack: M=128 descriptor over-read
+  L.bar = L.e + STAGES * E_STAGE;
+  L.tmem = L.bar + (2 * STAGES + 2) * 8;
+  L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
+  return L;
+}
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Parity wait with a watchdog: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  if (done) return;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int4 rows,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+// UMMA shared-memory matrix descriptor (tcgen05 format, version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                      // descriptor version (Blackwell)
+  d |= (uint64_t)(layout & 7) << 61;           // 0 = none, 2 = 128B swizzle
+  return d;
+}
+
+// Instruction descriptor: sparse kind::f16, BF16 x BF16 -> F32, A K-major, B MN-major.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 2)                 // sparse
+         | (1u << 4)               // D = F32
+         | (1u << 7)               // A = BF16
+         | (1u << 10)              // B = BF16
+         | (0u << 15)              // A K-major
+         | (1u << 16)              // B MN-major
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_sp(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t tmem_e, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(tmem_e)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo_f32), __uint_as_float(hi_f32));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ------------------------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const SmemLayout L = smem_layout(p.V);
+  const int V = p.V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
+  const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
+  const uint32_t bar_acc_full = bar_empty + STAGES * 8, bar_acc_empty = bar_acc_full + 8;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
+  const int n_epi_warps = V >= 128 ? 4 : V / 32;  // warps whose TMEM lane quadrant holds rows
+
+  // constant metadata for rows >= V in every E slot (never overwritten by the producer)
+  for (int i = threadIdx.x; i < STAGES * (128 - V) * 4; i += NUM_THREADS) {
+    const int s = i / ((128 - V) * 4), w = i % ((128 - V) * 4);
+    reinterpret_cast<uint32_t*>(gbase + L.e + s * E_STAGE + V * 16)[w] = META_PAD;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    mbar_init(bar_acc_full, 1);
+    mbar_init(bar_acc_empty, n_epi_warps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  const int T = p.T;
+  if (warp == 0) {
+    // ======================================================================== producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int t = u % T, nb = u / T;
+      const int k0 = p.tile_kofs[t], kp = p.tile_kofs[t + 1] - k0;
+      const int e0 = p.tile_eofs[t];
+      const int col0 = nb * BN;
+      for (int s = 0; s < kp / BK; ++s) {
+        int4 rows = make_int4(0, 0, 0, 0);
+        if (lane < 16) rows = reinterpret_cast<const int4*>(p.gidx + k0 + s * BK)[lane];
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        const uint32_t fb = bar_full + 8 * stage;
+        if (lane == 0) {
+          const uint32_t a_bytes = V * 64, e_bytes = (s & 1) ? 0 : V * 16;
+          mbar_expect_tx(fb, B_STAGE + a_bytes + e_bytes);
+          bulk_g2s(sA + stage * V * 64, p.a_vals + (int64_t)(k0 + s * BK) * V / 2, a_bytes, fb);
+          if (e_bytes)
+            bulk_g2s(sE + stage * E_STAGE, p.a_meta + ((int64_t)e0 + s / 2) * V * 4, e_bytes, fb);
+        }
+        __syncwarp();
+        if (lane < 16) {
+#pragma unroll
+          for (int q = 0; q < BN / 64; ++q)
+            tma_gather4(sB + stage * B_STAGE + q * (B_STAGE / 4) + lane * 512, &xmap, col0 + q * 64,
+                        rows, fb);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(128, BN);
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0, eslot = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int t = u % T;
+        const int kp = p.tile_kofs[t + 1] - p.tile_kofs[t];
+        if (kp == 0) continue;
+        mbar_wait(bar_acc_empty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int s = 0; s < kp / BK; ++s) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          tc_fence_after();
+          if ((s & 1) == 0) {
+            eslot = (eslot + 1) % E_SLOTS;
+            // 128 lanes x 16 B: K-major no-swizzle core matrices, 8-row groups at 128 B
+            tmem_cp_128x128b(tmem + E_COL + eslot * 4, smem_desc(sE + stage * E_STAGE, 0, 128, 0));
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2 + j;
+            const uint64_t a_desc = smem_desc(sA + stage * V * 64 + j * 32 * V, 128, 256, 0);
+            const uint64_t b_desc = smem_desc(sB + stage * B_STAGE + j * 4096, B_STAGE / 4, 1024, 2);
+            mma_sp(tmem, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
+          }
+          tc_commit(bar_empty + 8 * stage);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(bar_acc_full);
+        acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================================================================== epilogue
+    const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
+    if (q < n_epi_warps) {
+      uint32_t acc_phase = 0;
+      const int r = q * 32 + lane;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int t = u % T, nb = u / T;
+        const int kp = p.tile_kofs[t + 1] - p.tile_kofs[t];
+        const int64_t prow = (int64_t)t * V + r;
+        const int64_t orow = p.out_order == HINM_ORDER_ORIGINAL ? p.sigma_o[prow] : prow;
+        uint16_t* yrow = p.Y + orow * p.ldy;
+        const int col_base = nb * BN;
+        if (kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
+          for (int c = 0; c < BN; c += 8)
+            if (col_base + c < p.B)
+              *reinterpret_cast<uint4*>(yrow + col_base + c) = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        mbar_wait(bar_acc_full, acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c * 32, v);
+          const int col = col_base + c * 32;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            if (col + h * 8 < p.B) {
+              uint4 o;
+              o.x = pack_bf16x2(v[h * 8 + 0], v[h * 8 + 1]);
+              o.y = pack_bf16x2(v[h * 8 + 2], v[h * 8 + 3]);
+              o.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
+              o.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
+              *reinterpret_cast<uint4*>(yrow + col + h * 8) = o;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_acc_empty);
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace sm100
+}  // namespace hinm
+
+// ------------------------------------------------------------------------------ host side
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)ptr;
+  }
+  return fn;
+}
+
+thread_local int g_last_launches = 0;
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace
+
+extern "C" int hinm_last_launch_count(void) { return g_last_launches; }
+
+extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t ldx, int B,
+                              uint16_t* Y, int64_t ldy, int out_order, void* stream) {
+  using namespace hinm::sm100;
+  g_last_launches = 0;
+  if (!pk || !X || !Y) return HINM_ERR_VALUE;
+  if (pk->N != 2 || pk->M != 4) return HINM_ERR_UNSUPPORTED;
+  if (pk->V != 32 && pk->V != 64 && pk->V != 128) return HINM_ERR_UNSUPPORTED;
+  if (!pk->gidx || !pk->a_vals || !pk->a_meta || !pk->tile_kofs) return HINM_ERR_VALUE;
+  if (B < 0 || (B % 8) || (ldx % 8) || (ldy % 8) || ldx < B || ldy < B) return HINM_ERR_VALUE;
+  if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15)) return HINM_ERR_VALUE;
+  if (B == 0 || pk->m == 0) return HINM_OK;
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return HINM_ERR_CUDA;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)pk->n};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)X, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    fprintf(stderr, "[hinm] cuTensorMapEncodeTiled failed (%d)\n", (int)cr);
+    return HINM_ERR_CUDA;
+  }
+  Params prm;
+  prm.tile_kofs = pk->tile_kofs;
+  prm.tile_eofs = pk->tile_eofs;
+  prm.gidx = pk->gidx;
+  prm.a_vals = pk->a_vals;
+  prm.a_meta = pk->a_meta;
+  prm.sigma_o = pk->sigma_o;
+  prm.Y = Y;
+  prm.ldy = ldy;
+  prm.B = B;
+  prm.T = pk->T;
+  prm.V = pk->V;
+  const int nbk = (B + BN - 1) / BN;
+  prm.units = nbk * pk->T;
+  prm.out_order = out_order;
+  const SmemLayout L = smem_layout(pk->V);
+  HINM_CUDA_TRY(cudaFuncSetAttribute(k_hinm_spmm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)L.total));
+  const int grid = std::min(prm.units, sm_count());
+  k_hinm_spmm<<<grid, NUM_THREADS, L.total, (cudaStream_t)stream>>>(map, prm);
+  HINM_LAUNCH_CHECK();
+  g_last_launches = 1;
+  return HINM_OK;
+}

@@ -1,0 +1,269 @@
+"""Device-level API: the fused GPU compressor, the device pack and the tcgen05 SpMM.
+
+PyTorch is used only as plumbing (device memory, streams); all compute runs in
+libhinm_b200.so through the C ABI.  Every function raises instead of falling back to a CPU
+path when the library or a CUDA device is unavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError, ShapeMismatch
+from .model import HiNMConfig, ValidatedConfig, ensure_validated
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_handle(device=None) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _require_cuda(t, name: str):
+    if not (hasattr(t, "is_cuda") and t.is_cuda):
+        raise DeviceError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+@dataclass
+class DevicePack:
+    """A compressed HiNM matrix resident in HBM (reference view + tcgen05 operand image)."""
+
+    m: int
+    n: int
+    V: int
+    N: int
+    M: int
+    total_keep: int
+    config: HiNMConfig
+    sigma_o: object           # int32 [m]
+    tile_ptr: object          # int32 [T+1]
+    vec_idx: object           # int32 [K]
+    nm_pos: object            # uint8 [V*K/M*N]
+    kept: object              # bf16  [V*K/M*N]
+    tile_kofs: object = None  # int32 [T+1]
+    tile_eofs: object = None  # int32 [T+1]
+    gidx: object = None       # int32 [kpad_cap]
+    a_vals: object = None     # bf16  [V*kpad_cap/2]
+    a_meta: object = None     # int32 [meta words]
+    kpad_cap: int = 0
+    meta_cap: int = 0
+
+    @property
+    def T(self) -> int:
+        return self.m // self.V
+
+    @property
+    def device(self):
+        return self.vec_idx.device
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.m, self.n)
+
+    def struct(self) -> _lib.PackStruct:
+        s = _lib.PackStruct()
+        s.m, s.n, s.V, s.N, s.M, s.T = self.m, self.n, self.V, self.N, self.M, self.T
+        s.total_keep = self.total_keep
+        s.tile_ptr, s.vec_idx = _ptr(self.tile_ptr), _ptr(self.vec_idx)
+        s.nm_pos, s.kept_bf16, s.sigma_o = _ptr(self.nm_pos), _ptr(self.kept), _ptr(self.sigma_o)
+        s.kpad_cap, s.meta_words_cap = self.kpad_cap, self.meta_cap
+        s.tile_kofs, s.tile_eofs = _ptr(self.tile_kofs), _ptr(self.tile_eofs)
+        s.gidx, s.a_vals, s.a_meta = _ptr(self.gidx), _ptr(self.a_vals), _ptr(self.a_meta)
+        return s
+
+    @property
+    def has_operand_image(self) -> bool:
+        return self.a_vals is not None
+
+    def nbytes_operand_image(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in
+                   (self.gidx, self.a_vals, self.a_meta) if t is not None)
+
+    # -------------------------------------------------------------------- reference view
+    def to_host_tiles(self):
+        """[(vector_index int64, nm_index (V, G*N) int64, kept_values (V, G*N) float64)] per tile."""
+        torch = _torch()
+        tp = self.tile_ptr.cpu().numpy().astype(np.int64)
+        vi = self.vec_idx.cpu().numpy().astype(np.int64)
+        nm = self.nm_pos.cpu().numpy().astype(np.int64)
+        kv = self.kept.float().cpu().numpy().astype(np.float64)
+        V, N, M = self.V, self.N, self.M
+        out = []
+        for t in range(self.T):
+            k = int(tp[t + 1] - tp[t])
+            b = V * (int(tp[t]) // M) * N
+            w = k // M * N
+            out.append((vi[tp[t]:tp[t + 1]].copy(), nm[b:b + V * w].reshape(V, w),
+                        kv[b:b + V * w].reshape(V, w)))
+        del torch
+        return out
+
+    def replicate(self, device) -> "DevicePack":
+        """Copy of the pack on another device (weights are replicated for token sharding)."""
+        fields = {}
+        for name in ("sigma_o", "tile_ptr", "vec_idx", "nm_pos", "kept", "tile_kofs", "tile_eofs",
+                     "gidx", "a_vals", "a_meta"):
+            t = getattr(self, name)
+            fields[name] = None if t is None else t.to(device, non_blocking=True)
+        return DevicePack(self.m, self.n, self.V, self.N, self.M, self.total_keep, self.config,
+                          kpad_cap=self.kpad_cap, meta_cap=self.meta_cap, **fields)
+
+
+def _alloc_operand_image(pack: DevicePack) -> None:
+    torch = _torch()
+    lib = _lib.load()
+    kc, mc, ac = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(lib.hinm_pack_capacity(pack.m, pack.n, pack.V, pack.total_keep, ctypes.byref(kc),
+                                      ctypes.byref(mc), ctypes.byref(ac)), "pack_capacity")
+    dev = pack.vec_idx.device
+    T = pack.T
+    pack.kpad_cap, pack.meta_cap = kc.value, mc.value
+    pack.tile_kofs = torch.empty(T + 1, dtype=torch.int32, device=dev)
+    pack.tile_eofs = torch.empty(T + 1, dtype=torch.int32, device=dev)
+    pack.gidx = torch.empty(kc.value, dtype=torch.int32, device=dev)
+    pack.a_vals = torch.empty(ac.value, dtype=torch.bfloat16, device=dev)
+    pack.a_meta = torch.empty(mc.value, dtype=torch.int32, device=dev)
+
+
+def spmm_supported(V: int, N: int, M: int) -> bool:
+    return N == 2 and M == 4 and V in (32, 64, 128)
+
+
+def _empty_pack(vcfg: ValidatedConfig, device) -> DevicePack:
+    torch = _torch()
+    V, N, M = vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group
+    K = vcfg.total_keep
+    L = V * K // M * N
+    return DevicePack(
+        vcfg.rows, vcfg.cols, V, N, M, K, vcfg.config,
+        sigma_o=torch.empty(vcfg.rows, dtype=torch.int32, device=device),
+        tile_ptr=torch.empty(vcfg.num_tiles + 1, dtype=torch.int32, device=device),
+        vec_idx=torch.empty(max(K, 1), dtype=torch.int32, device=device),
+        nm_pos=torch.empty(max(L, 1), dtype=torch.uint8, device=device),
+        kept=torch.empty(max(L, 1), dtype=torch.bfloat16, device=device))
+
+
+def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None):
+    """Fused GPU compressor (north-star subsystem 1): bf16 W (m x n, CUDA) + sigma -> DevicePack.
+
+    ``sigma_o``: permutation of the m output channels; ``sigma_i``: optional per-tile gather
+    orders (must be permutations of each tile's survivors, else InvariantViolation); default
+    ascending survivors.  Bit-exact with the reference's vector_prune -> nm_prune -> encode.
+    """
+    torch = _torch()
+    _require_cuda(weights, "weights")
+    if weights.dtype != torch.bfloat16 or weights.dim() != 2:
+        raise ValueError("weights must be a 2-D bfloat16 CUDA tensor")
+    m, n = weights.shape
+    vcfg = ensure_validated(cfg, (m, n))
+    dev = weights.device
+    so = torch.as_tensor(np.asarray(sigma_o), dtype=torch.int32).to(dev) if not (
+        hasattr(sigma_o, "is_cuda")) else sigma_o.to(device=dev, dtype=torch.int32)
+    if so.numel() != m:
+        raise ShapeMismatch(f"sigma_o has {so.numel()} entries, weights have {m} rows")
+    pack = _empty_pack(vcfg, dev)
+    pack.sigma_o = so.contiguous()
+    if build_operand_image is None:
+        build_operand_image = spmm_supported(vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group)
+    if build_operand_image:
+        _alloc_operand_image(pack)
+    lib = _lib.load()
+    ws_bytes = ctypes.c_size_t()
+    _lib.check(lib.hinm_compress_workspace(m, n, vcfg.vector_size, vcfg.nm_group,
+                                           ctypes.byref(ws_bytes)), "compress_workspace")
+    ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=dev)
+    vmask = torch.empty(vcfg.num_tiles * n, dtype=torch.uint8, device=dev)
+    sp = si = None
+    if sigma_i is not None:
+        sizes = [len(s) for s in sigma_i]
+        if len(sizes) != vcfg.num_tiles:
+            raise ShapeMismatch(f"sigma_i has {len(sizes)} tiles, expected {vcfg.num_tiles}")
+        ptr = np.zeros(len(sizes) + 1, dtype=np.int64)
+        ptr[1:] = np.cumsum(sizes)
+        if ptr[-1] != vcfg.total_keep:
+            from .errors import InvariantViolation
+            raise InvariantViolation("sigma_i does not match the tiles' surviving vectors")
+        sp = torch.as_tensor(ptr.astype(np.int32)).to(dev)
+        flat = np.concatenate([np.asarray(s, dtype=np.int64) for s in sigma_i]) if sizes else \
+            np.empty(0, np.int64)
+        si = torch.as_tensor(flat.astype(np.int32)).to(dev)
+    st = pack.struct()
+    with torch.cuda.device(dev):
+        status = lib.hinm_compress_bf16(weights.data_ptr(), weights.stride(0), pack.sigma_o.data_ptr(),
+                                        _ptr(sp), _ptr(si), ctypes.byref(st), vmask.data_ptr(),
+                                        ws.data_ptr(), ws_bytes.value, _stream_handle(dev))
+    _lib.check(status, "compress")
+    pack.vector_mask = vmask.view(vcfg.num_tiles, n)
+    return pack
+
+
+def build_operand_image(pack: DevicePack) -> DevicePack:
+    """(Re)build the tcgen05 operand image of a pack from its reference view."""
+    torch = _torch()
+    if not spmm_supported(pack.V, pack.N, pack.M):
+        raise ValueError(f"SpMM supports 2:4 with V in (32, 64, 128); got V={pack.V}, "
+                         f"{pack.N}:{pack.M}")
+    if pack.a_vals is None:
+        _alloc_operand_image(pack)
+    st = pack.struct()
+    with torch.cuda.device(pack.device):
+        _lib.check(_lib.load().hinm_pack_build(ctypes.byref(st), _stream_handle(pack.device)),
+                   "pack_build")
+    return pack
+
+
+def spmm(pack: DevicePack, X, out=None, order: str = "sigma"):
+    """tcgen05 HiNM SpMM: Y (m x B, bf16) = W_hinm @ X (n x B, bf16, channel-major).
+
+    ``order='sigma'`` returns rows in sigma_o order (== hinm.hinm_spmm); ``'original'`` fuses
+    restore_row_order into the epilogue store.
+    """
+    torch = _torch()
+    _require_cuda(X, "inputs")
+    if X.dtype != torch.bfloat16 or X.dim() != 2:
+        raise ValueError("inputs must be a 2-D bfloat16 CUDA tensor")
+    if X.shape[0] != pack.n:
+        raise ShapeMismatch(f"input has {X.shape[0]} rows, encoding expects {pack.n}")
+    if not pack.has_operand_image:
+        raise ValueError("pack has no tcgen05 operand image (needs 2:4 and V in 32/64/128)")
+    B = X.shape[1]
+    if out is None:
+        out = torch.empty(pack.m, B, dtype=torch.bfloat16, device=X.device)
+    ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
+    st = pack.struct()
+    lib = _lib.load()
+    status = lib.hinm_spmm_bf16(ctypes.byref(st), X.data_ptr(), X.stride(0), B, out.data_ptr(),
+                                out.stride(0), ordv, _stream_handle(X.device))
+    _lib.check(status, "spmm")
+    return out
+
+
+def spmm_simt(pack: DevicePack, X, order: str = "sigma"):
+    """Cross-check product on CUDA cores from the reference view (fp32 out)."""
+    torch = _torch()
+    _require_cuda(X, "inputs")
+    if X.shape[0] != pack.n:
+        raise ShapeMismatch(f"input has {X.shape[0]} rows, encoding expects {pack.n}")
+    B = X.shape[1]
+    out = torch.zeros(pack.m, B, dtype=torch.float32, device=X.device)
+    ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
+    st = pack.struct()
+    _lib.check(_lib.load().hinm_spmm_simt_f32(ctypes.byref(st), X.data_ptr(), X.stride(0), B,
+                                              out.data_ptr(), out.stride(0), ordv,
+                                              _stream_handle(X.device)), "spmm_simt")
+    return out
