@@ -1,0 +1,368 @@
+"""Benchmark: HiNM SpMM effective TFLOPS and speed-up vs cuBLAS dense bf16 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the headline target): one LLaMA-7B FFN layer at 75% HiNM
+sparsity (V=64, 2:4, s_v=0.5) on 16384 tokens -- gate + up (11008x4096) and down
+(4096x11008) SpMMs per step, the down projection consuming the up projection's output in
+original channel order (the sigma_o restore is fused in the epilogue).  Token-sharded over N
+GPUs with replicated packed weights and no collective in the timed region (strong scaling:
+global tokens fixed).  Synthetic N(0,1) bf16 weights/activations, seeded; random sigma_o.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+The reference arm (--impl reference) times the CPU oracle port of the reference's hinm_spmm
+(oracle/hinm_oracle.py, gather + per-row GEMV in float64, all host BLAS threads) on a bounded
+sample of the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_FFN, N_FFN = 11008, 4096
+V, NM_N, NM_M, SV = 64, 2, 4, 0.5
+GLOBAL_TOKENS = 16384
+METRIC = "HiNM SpMM effective TFLOPS (LLaMA-7B FFN gate+up+down, 75% HiNM V=64 2:4)"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def layer_shapes():
+    # (name, m, n): gate, up: 11008 x 4096; down: 4096 x 11008
+    return [("gate", M_FFN, N_FFN), ("up", M_FFN, N_FFN), ("down", N_FFN, M_FFN)]
+
+
+def eff_flops(tokens):
+    return sum(2.0 * m * n * tokens for _, m, n in layer_shapes())
+
+
+def sparse_flops(tokens):
+    return sum(2.0 * m * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_20496_b200 as H
+    from paper_2407_20496_b200 import _lib
+    from paper_2407_20496_b200.build import build as _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        _build(force=False, verbose=False)
+    if world > 1:
+        dist.barrier()
+    lib = _lib.load()
+
+    tokens = GLOBAL_TOKENS // world                      # token shard of this rank
+    cfg = H.HiNMConfig(V, NM_N, NM_M, SV)
+    g = torch.Generator(device=dev)
+    packs, dense = {}, {}
+    comp_ms = {}
+    for i, (name, m, n) in enumerate(layer_shapes()):
+        g.manual_seed(1000 + i)                          # same weights on every rank (replicated)
+        W = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        so = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
+        H.compress(W, cfg, so)                           # warm-up (allocator, cub, attributes)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        packs[name] = H.compress(W, cfg, so)
+        torch.cuda.synchronize()
+        comp_ms[name] = (time.perf_counter() - t0) * 1e3
+        dense[name] = W
+    g.manual_seed(7 + rank)
+    X = torch.randn(N_FFN, tokens, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    y_gate = torch.empty(M_FFN, tokens, dtype=torch.bfloat16, device=dev)
+    y_up = torch.empty(M_FFN, tokens, dtype=torch.bfloat16, device=dev)
+    y_down = torch.empty(N_FFN, tokens, dtype=torch.bfloat16, device=dev)
+
+    def step(x):
+        H.spmm(packs["gate"], x, out=y_gate, order="original")
+        H.spmm(packs["up"], x, out=y_up, order="original")
+        H.spmm(packs["down"], y_up, out=y_down, order="original")
+        return y_down
+
+    def timed(fn, iters):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step(X)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms_total = timed(lambda: step(X), args.steps)
+    launches = 3 * args.steps                            # hinm_spmm_bf16 launches one kernel each
+    assert lib.hinm_last_launch_count() == 1
+    ms_step = ms_total / args.steps
+    value = eff_flops(GLOBAL_TOKENS) / (ms_step * 1e-3) / 1e12
+
+    # per-kernel (roofline) and cuBLAS dense comparator on the same shapes
+    per_kernel = {}
+    cublas = {}
+    for name, m, n in layer_shapes():
+        xin = X if name != "down" else y_up
+        out = y_down if name == "down" else y_up
+        for _ in range(3):
+            H.spmm(packs[name], xin, out=out, order="original")
+        ms_k = timed(lambda: H.spmm(packs[name], xin, out=out, order="original"), args.steps) / args.steps
+        per_kernel[name] = ms_k
+        Wd = dense[name]
+        for _ in range(3):
+            torch.matmul(Wd, xin)
+        cublas[name] = timed(lambda: torch.matmul(Wd, xin), args.steps) / args.steps
+    ms_cublas_step = sum(cublas.values())
+    cublas_tflops = eff_flops(GLOBAL_TOKENS) / (ms_cublas_step * 1e-3) / 1e12
+
+    # end to end through the public API: pinned host X in, Y_down out, every step
+    xh = X.cpu().pin_memory()
+    yh = torch.empty(N_FFN, tokens, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        xd = xh.to(dev, non_blocking=True)
+        y = step(xd)
+        yh.copy_(y, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    ms_e2e = timed(e2e_step, args.steps) / args.steps
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    pk, kind = peaks()
+    p_sparse = 2.0 * pk["bf16_tflops"]
+    f_sp = sparse_flops(GLOBAL_TOKENS // world)
+    achieved = f_sp / (sum(per_kernel.values()) * 1e-3) / 1e12
+    comp_bytes = 0
+    for name, m, n in layer_shapes():
+        kbar = int(n * (1 - SV))
+        comp_bytes += 2 * m * n + m * kbar + m * kbar // 8 + 4 * (m // V) * kbar + 4 * m
+    result = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) bf16 weights/activations, random sigma_o)",
+        "config": {
+            "workload": "LLaMA-7B FFN layer (gate+up 11008x4096, down 4096x11008), 75% HiNM "
+                        "V=64 2:4 s_v=0.5, 16384 tokens token-sharded",
+            "global_tokens": GLOBAL_TOKENS, "tokens_per_gpu": GLOBAL_TOKENS // world,
+            "parallelism": f"token-shard x{world}, weights replicated, no collective",
+            "l2": "inputs larger than L2 (X 134 MB + 3 packs ~150 MB per step at N=1)",
+        },
+        "speedup_vs_cublas": round(ms_cublas_step / ms_step, 3),
+        "cublas_dense_bf16": {"tflops": round(cublas_tflops, 2), "ms_per_step": round(ms_cublas_step, 4),
+                              "per_gemm_ms": {k: round(v, 4) for k, v in cublas.items()}},
+        "per_spmm_ms": {k: round(v, 4) for k, v in per_kernel.items()},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(p_sparse, 1),
+                     "unit": "TFLOP/s", "frac": round(achieved / p_sparse, 4), "traffic": None,
+                     "peak_source": f"2 x bf16_tflops of {kind} MEASURED_PEAKS.json (2:4 sparse)",
+                     "algorithmic": "2*m*k_bar*tokens per SpMM (k_bar = n/2 kept vectors)"},
+        "compressor": {"ms": {k: round(v, 3) for k, v in comp_ms.items()},
+                       "algorithmic_bytes": comp_bytes,
+                       "gbs": round(comp_bytes / (sum(comp_ms.values()) * 1e-3) / 1e9, 1),
+                       "note": "host wall time incl. sigma validation sync, 3 layers"},
+        "e2e": {"value": round(eff_flops(GLOBAL_TOKENS) / (ms_e2e * 1e-3) / 1e12, 2),
+                "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),
+                "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(packs["down"], args.cpu_tokens)
+    print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(pack, tokens: int):
+    """Oracle port of hinm_spmm (float64 gather + GEMV, host BLAS) on a bounded token sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hinm_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:  # pragma: no cover
+        blas_threads = os.cpu_count()
+    tiles = pack.to_host_tiles()
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((pack.n, tokens)).astype(np.float32).astype(np.float64)
+    t0 = time.perf_counter()
+    Y = O.hinm_spmm(tiles, X, pack.m, pack.V, pack.N, pack.M)
+    O.restore_row_order(Y, pack.sigma_o.cpu().numpy())
+    dt = time.perf_counter() - t0
+    f = 2.0 * pack.m * pack.n * tokens
+    return {"value": round(f / dt / 1e12, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
+            "kind": "port", "seconds": round(dt, 2),
+            "sample": f"down projection 4096x11008 (V=64 2:4), {tokens} tokens, oracle "
+                      f"hinm_spmm + restore_row_order, float64; host cpu_count={os.cpu_count()}"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on the same workload (bounded samples), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hinm_oracle as O
+    from paper_2407_20496_b200 import synth
+
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:  # pragma: no cover
+        blas_threads = os.cpu_count()
+    m, n = N_FFN, M_FFN                          # down projection is the sample layer
+    W = synth.randn_bf16((m, n), 0).astype(np.float64)
+    so = synth.random_sigma_o(m, 2)
+    r = O.compress(W, so, V, NM_N, NM_M, (m // V) * int(n * (1 - SV)))
+    tokens = args.cpu_tokens
+    X = synth.randn_bf16((n, tokens), 1).astype(np.float64)
+
+    def one():
+        Y = O.hinm_spmm(r["tiles"], X, m, V, NM_N, NM_M)
+        O.restore_row_order(Y, so)
+
+    for _ in range(min(args.warmup, 1)):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 2.0 * m * n * tokens / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "LLaMA-7B FFN down projection sample (4096x11008, V=64 2:4, "
+                               f"{tokens} tokens) of the bench workload"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
+                         "kind": "port",
+                         "sample": f"oracle hinm_spmm + restore_row_order, {tokens} tokens per step"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-tokens", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -182,11 +182,15 @@ def test_errors_follow_reference():
     bad[1] = np.array(sorted(set(range(16)) - set(surv[1].tolist()))[: surv[1].size])
     with pytest.raises(H.InvariantViolation):
         H.nm_prune(S, vm, cfg, H.GyroPermutation(np.arange(8), tuple(bad)))
-    # k_t % M != 0 with a matching sigma_i -> GroupingError (test_pruning.py:205-211 shape)
-    cfg1 = H.HiNMConfig(1, 2, 4, 0.0)
+    # k_t % M != 0 with a matching sigma_i -> GroupingError (pruning.py:201-204); the
+    # reference test at test_pruning.py:205-211 is known-bad (DimensionError fires first)
+    cfg1 = H.HiNMConfig(1, 2, 4, 0.5)
+    vm1 = np.zeros((2, 8), bool)
+    vm1[0, :6] = True
+    vm1[1, :2] = True
     with pytest.raises(H.GroupingError):
-        H.nm_prune(np.ones((1, 6)), np.ones((1, 6), bool), cfg1,
-                   H.GyroPermutation(np.array([0]), (np.arange(6),)))
+        H.nm_prune(np.ones((2, 8)), vm1, cfg1,
+                   H.GyroPermutation(np.arange(2), (np.arange(6), np.arange(2))))
     # encode with an element kept inside a pruned vector (test_pruning.py:239-246)
     cfg2 = H.HiNMConfig(2, 1, 2, 0.5)
     W2 = synth.randn_bf16((4, 4), 4).astype(np.float64)
