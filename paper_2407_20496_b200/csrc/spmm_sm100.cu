@@ -22,6 +22,7 @@
 // max(M,128)*N/256), so this costs smem read bandwidth only.
 #include <cuda.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -288,44 +289,81 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     }
   } else if (warp >= GATHER_WARP0) {
     // ============================================================ gather producers
+    // Flattened stream over (unit, stage); the gather indices of stage i+PF are loaded while
+    // stage i is issued, so the dependent index load never sits on the critical path.
     const int gw = warp - GATHER_WARP0;
+    constexpr int PF = 4;
+    constexpr int RPW = BK / GW;             // K-rows per warp per stage (cp.async mode)
+    // prefetch cursor
+    int pu = blockIdx.x, ps = 0, pk0 = 0, pnst = 0;
+    auto load_unit = [&](int u) {
+      while (u < p.units) {
+        const int t = u % T;
+        pk0 = __ldg(p.tile_kofs + t);
+        pnst = (__ldg(p.tile_kofs + t + 1) - pk0) / BK;
+        if (pnst > 0) break;
+        u += gridDim.x;
+      }
+      pu = u;
+      ps = 0;
+    };
+    load_unit(pu);
+    int r_row[PF], r_col[PF];
+    int4 r_quad[PF];
+    bool r_ok[PF];
+    auto prefetch = [&](int slot) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        if (j != slot) continue;
+        r_ok[j] = pu < p.units;
+        if (!r_ok[j]) return;
+        r_col[j] = (pu / T) * BN;
+        const int* gi = p.gidx + pk0 + ps * BK;
+        if (MODE == GATHER_CPASYNC) {
+          r_row[j] = lane < RPW ? __ldg(gi + gw + lane * GW) : 0;
+        } else {
+          const int g = gw * 32 + lane;
+          r_quad[j] = g < 64 ? __ldg(reinterpret_cast<const int4*>(gi) + (g >> 2)) : make_int4(0, 0, 0, 0);
+        }
+        if (++ps == pnst) load_unit(pu + gridDim.x);
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < PF; ++j) prefetch(j);
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int t = u % T, nb = u / T;
-      const int k0 = p.tile_kofs[t], kp = p.tile_kofs[t + 1] - k0;
-      const int col0 = nb * BN;
-      for (int s = 0; s < kp / BK; ++s) {
-        const int* gi = p.gidx + k0 + s * BK;
+    bool done = false;
+    while (!done) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        if (!r_ok[j]) { done = true; break; }
+        const int col0 = r_col[j];
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         if (MODE == GATHER_CPASYNC) {
-          // this warp copies K-rows r = gw, gw+GW, ...; lane = 16-byte chunk of the 512-byte row
-          constexpr int RPW = BK / GW;
-          int my_row = lane < RPW ? gi[gw + lane * GW] : 0;
           const int tok = col0 + lane * 8;
           const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-          const int nbk = lane >> 3, j = lane & 7;
-          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-          const uint32_t sb = sB + stage * B_STAGE + nbk * (B_STAGE / 4);
+          const uint16_t* xs = X + (src_bytes ? tok : 0);
+          const int j8 = lane & 7;
+          const uint32_t sb = sB + stage * B_STAGE + (lane >> 3) * (B_STAGE / 4);
+          const int my_row = r_row[j];
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
             const int r = gw + i * GW;
             const int row = __shfl_sync(0xffffffffu, my_row, i);
-            const uint32_t dst = sb + (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4);
-            cp_async_16(dst, X + (int64_t)row * ldx + (src_bytes ? tok : 0), src_bytes);
+            const uint32_t dst = sb + (r >> 3) * 1024 + (r & 7) * 128 + ((j8 ^ (r & 7)) << 4);
+            cp_async_16(dst, xs + (int64_t)row * ldx, src_bytes);
           }
           cp_async_arrive_noinc(bar_full + 8 * stage);
         } else {
-          // TMA gather4: 16 quads of rows x 4 token sub-blocks, spread over the gather warps
-          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-          const uint32_t fb = bar_full + 8 * stage;
-          for (int g = gw * 32 + lane; g < 64; g += GW * 32) {
+          const int g = gw * 32 + lane;
+          if (g < 64) {
             const int quad = g >> 2, q = g & 3;
-            const int4 rows = reinterpret_cast<const int4*>(gi)[quad];
-            tma_gather4(sB + stage * B_STAGE + q * (B_STAGE / 4) + quad * 512, &xmap, col0 + q * 64,
-                        rows, fb);
+            tma_gather4(sB + stage * B_STAGE + q * (B_STAGE / 4) + quad * 512, &xmap,
+                        col0 + q * 64, r_quad[j], bar_full + 8 * stage);
           }
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        prefetch(j);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -495,20 +533,29 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   prm.out_order = out_order;
   const SmemLayout L = smem_layout(pk->V);
   const int grid = std::min(prm.units, sm_count());
-  static const int mode = [] {
+  // variant: cp.async gather with 4 (default) or 8 warps, or TMA gather4 with 2 / 4 warps
+  static const int variant = [] {
     const char* e = getenv("HINM_GATHER");
-    return (e && e[0] == 't') ? (int)GATHER_TMA : (int)GATHER_CPASYNC;
+    if (!e) return 0;
+    if (!strcmp(e, "cp8")) return 1;
+    if (!strcmp(e, "tma") || !strcmp(e, "tma2")) return 2;
+    if (!strcmp(e, "tma4")) return 3;
+    return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
-  if (mode == GATHER_TMA) {
-    auto kern = k_hinm_spmm<GATHER_TMA, 2>;
+  auto launch = [&](auto kern, int gw) -> int {
     HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<grid, 32 * (GATHER_WARP0 + 2), L.total, st>>>(map, X, ldx, prm);
-  } else {
-    auto kern = k_hinm_spmm<GATHER_CPASYNC, 4>;
-    HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<grid, 32 * (GATHER_WARP0 + 4), L.total, st>>>(map, X, ldx, prm);
+    kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(map, X, ldx, prm);
+    return HINM_OK;
+  };
+  int rc;
+  switch (variant) {
+    case 1: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
+    case 2: rc = launch(k_hinm_spmm<GATHER_TMA, 2>, 2); break;
+    case 3: rc = launch(k_hinm_spmm<GATHER_TMA, 4>, 4); break;
+    default: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 4>, 4); break;
   }
+  if (rc) return rc;
   HINM_LAUNCH_CHECK();
   g_last_launches = 1;
   return HINM_OK;
