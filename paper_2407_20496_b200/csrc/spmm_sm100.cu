@@ -289,25 +289,30 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     }
   } else if (warp >= GATHER_WARP0) {
     // ============================================================ gather producers
-    // Flattened stream over (unit, stage); the gather indices of stage i+PF are loaded while
-    // stage i is issued, so the dependent index load never sits on the critical path.
+    // Flattened stream over (unit, stage) with the gather indices of stage i+PF loaded while
+    // stage i is issued (the dependent index load never sits on the critical path).  The
+    // issue loop is kept to ~4 instructions per 512-byte row: warp gw owns the K-rows
+    // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.
     const int gw = warp - GATHER_WARP0;
     constexpr int PF = 4;
-    constexpr int RPW = BK / GW;             // K-rows per warp per stage (cp.async mode)
-    // prefetch cursor
-    int pu = blockIdx.x, ps = 0, pk0 = 0, pnst = 0;
-    auto load_unit = [&](int u) {
-      while (u < p.units) {
-        const int t = u % T;
-        pk0 = __ldg(p.tile_kofs + t);
-        pnst = (__ldg(p.tile_kofs + t + 1) - pk0) / BK;
+    constexpr int RPW = BK / GW;  // K-rows per warp per stage
+    static_assert(MODE == GATHER_TMA || GW == 8, "cp.async producer assumes 8 gather warps");
+    const int dt = gridDim.x % T, dnb = gridDim.x / T;
+    // prefetch cursor: unit (pt, pnb) with running index pu, stage ps of pnst
+    int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pnst = 0;
+    auto next_unit = [&]() {  // advance to the next unit with work
+      while (pu < p.units) {
+        pk0 = __ldg(p.tile_kofs + pt);
+        pnst = (__ldg(p.tile_kofs + pt + 1) - pk0) / BK;
         if (pnst > 0) break;
-        u += gridDim.x;
+        pu += gridDim.x;
+        pt += dt;
+        pnb += dnb;
+        if (pt >= T) { pt -= T; ++pnb; }
       }
-      pu = u;
       ps = 0;
     };
-    load_unit(pu);
+    next_unit();
     int r_row[PF], r_col[PF];
     int4 r_quad[PF];
     bool r_ok[PF];
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (j != slot) continue;
         r_ok[j] = pu < p.units;
         if (!r_ok[j]) return;
-        r_col[j] = (pu / T) * BN;
+        r_col[j] = pnb * BN;
         const int* gi = p.gidx + pk0 + ps * BK;
         if (MODE == GATHER_CPASYNC) {
           r_row[j] = lane < RPW ? __ldg(gi + gw + lane * GW) : 0;
@@ -325,11 +330,21 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const int g = gw * 32 + lane;
           r_quad[j] = g < 64 ? __ldg(reinterpret_cast<const int4*>(gi) + (g >> 2)) : make_int4(0, 0, 0, 0);
         }
-        if (++ps == pnst) load_unit(pu + gridDim.x);
+        if (++ps == pnst) {
+          pu += gridDim.x;
+          pt += dt;
+          pnb += dnb;
+          if (pt >= T) { pt -= T; ++pnb; }
+          next_unit();
+        }
       }
     };
 #pragma unroll
     for (int j = 0; j < PF; ++j) prefetch(j);
+    // per-warp constant part of the SWIZZLE_128B destination (row r = gw + 8 i: r & 7 = gw)
+    const uint32_t dst_lane = (lane >> 3) * (B_STAGE / 4) + gw * 128 + (((lane & 7) ^ gw) << 4);
+    const char* xbase = reinterpret_cast<const char*>(X);
+    const int64_t ldx2 = ldx * 2;
     int stage = 0;
     uint32_t phase = 0;
     bool done = false;
@@ -342,16 +357,13 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (MODE == GATHER_CPASYNC) {
           const int tok = col0 + lane * 8;
           const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-          const uint16_t* xs = X + (src_bytes ? tok : 0);
-          const int j8 = lane & 7;
-          const uint32_t sb = sB + stage * B_STAGE + (lane >> 3) * (B_STAGE / 4);
+          const char* xs = xbase + (src_bytes ? (int64_t)tok * 2 : 0);
+          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
           const int my_row = r_row[j];
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
-            const int r = gw + i * GW;
             const int row = __shfl_sync(0xffffffffu, my_row, i);
-            const uint32_t dst = sb + (r >> 3) * 1024 + (r & 7) * 128 + ((j8 ^ (r & 7)) << 4);
-            cp_async_16(dst, xs + (int64_t)row * ldx, src_bytes);
+            cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
           }
           cp_async_arrive_noinc(bar_full + 8 * stage);
         } else {
@@ -553,7 +565,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 1: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
     case 2: rc = launch(k_hinm_spmm<GATHER_TMA, 2>, 2); break;
     case 3: rc = launch(k_hinm_spmm<GATHER_TMA, 4>, 4); break;
-    default: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 4>, 4); break;
+    default: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
   }
   if (rc) return rc;
   HINM_LAUNCH_CHECK();
