@@ -219,6 +219,27 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// Per-unit parameters.  Each role loads the NEXT unit's parameters while it works on the
+// current one: under load the SM's L1tex queue is full of gather traffic and a dependent
+// global load at a unit boundary would otherwise stall ~3k cycles.
+struct UnitParams {
+  int t, nb, k0, kp, e0;
+};
+
+__device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
+  UnitParams q;
+  if (u >= p.units) {
+    q.t = q.nb = q.k0 = q.kp = q.e0 = 0;
+    return q;
+  }
+  q.t = u % p.T;
+  q.nb = u / p.T;
+  q.k0 = __ldg(p.tile_kofs + q.t);
+  q.kp = __ldg(p.tile_kofs + q.t + 1) - q.k0;
+  q.e0 = __ldg(p.tile_eofs + q.t);
+  return q;
+}
+
 template <int MODE, int GW>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
@@ -271,10 +292,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      UnitParams nxt = unit_params(p, blockIdx.x);
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int t = u % T;
-        const int k0 = p.tile_kofs[t], kp = p.tile_kofs[t + 1] - k0;
-        const int e0 = p.tile_eofs[t];
+        const UnitParams cur = nxt;
+        nxt = unit_params(p, u + gridDim.x);
+        const int k0 = cur.k0, kp = cur.kp, e0 = cur.e0;
         for (int s = 0; s < kp / BK; ++s) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t fb = bar_full + 8 * stage;
@@ -294,7 +316,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     // issue loop is kept to ~4 instructions per 512-byte row: warp gw owns the K-rows
     // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.
     const int gw = warp - GATHER_WARP0;
-    constexpr int PF = 4;
+    constexpr int PF = 8;
     constexpr int RPW = BK / GW;  // K-rows per warp per stage
     static_assert(MODE == GATHER_TMA || GW == 8, "cp.async producer assumes 8 gather warps");
     const int dt = gridDim.x % T, dnb = gridDim.x / T;
@@ -384,9 +406,10 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       const uint32_t idesc = make_idesc(128, BN);
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0, eslot = 0;
+      UnitParams nxt = unit_params(p, blockIdx.x);
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int t = u % T;
-        const int kp = p.tile_kofs[t + 1] - p.tile_kofs[t];
+        const int kp = nxt.kp;
+        nxt = unit_params(p, u + gridDim.x);
         if (kp == 0) continue;
         mbar_wait(bar_acc_empty, acc_phase ^ 1);
         tc_fence_after();
@@ -419,11 +442,18 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     if (q < n_epi_warps) {
       uint32_t acc_phase = 0;
       const int r = q * 32 + lane;
+      auto out_row = [&](const UnitParams& q) -> int64_t {
+        const int64_t prow = (int64_t)q.t * V + r;
+        return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
+      };
+      UnitParams nxt = unit_params(p, blockIdx.x);
+      int64_t nxt_row = blockIdx.x < p.units ? out_row(nxt) : 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int t = u % T, nb = u / T;
-        const int kp = p.tile_kofs[t + 1] - p.tile_kofs[t];
-        const int64_t prow = (int64_t)t * V + r;
-        const int64_t orow = p.out_order == HINM_ORDER_ORIGINAL ? p.sigma_o[prow] : prow;
+        const UnitParams cur = nxt;
+        const int64_t orow = nxt_row;
+        nxt = unit_params(p, u + gridDim.x);
+        if (u + (int)gridDim.x < p.units) nxt_row = out_row(nxt);
+        const int nb = cur.nb, kp = cur.kp;
         uint16_t* yrow = p.Y + orow * p.ldy;
         const int col_base = nb * BN;
         if (kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
