@@ -193,6 +193,163 @@ __global__ void __launch_bounds__(NT) k_budget(const double* __restrict__ gains,
   if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
 }
 
+// a4 (fast path, n <= 16384): one CTA per tile sorts the tile's scores in registers/smem with a
+// stable block radix sort (descending keys; input in column order => ties keep the lower
+// column first, == np.lexsort((cols, -score))).
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_tile_sort(const double* __restrict__ scores, int n,
+                                                  double* __restrict__ sorted,
+                                                  int32_t* __restrict__ order) {
+  typedef cub::BlockRadixSort<double, NT, ITEMS, int32_t> BRS;
+  extern __shared__ __align__(16) uint8_t sort_smem[];
+  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(sort_smem);
+  const int t = blockIdx.x;
+  const double* row = scores + (int64_t)t * n;
+  double keys[ITEMS];
+  int32_t vals[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int j = threadIdx.x * ITEMS + i;  // blocked arrangement = column order
+    keys[i] = j < n ? row[j] : -INFINITY;
+    vals[i] = j;
+  }
+  BRS(tmp).SortDescending(keys, vals);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int j = threadIdx.x * ITEMS + i;
+    if (j < n) {
+      sorted[(int64_t)t * n + j] = keys[i];
+      order[(int64_t)t * n + j] = vals[i];
+    }
+  }
+}
+
+// a5 (fast path): exact radix select of the G-th smallest key d = ~bits(gain) over all tiles
+// (8-bit digits, per-warp histograms), then per-tile counts with the (q, t) tie order.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ gains, int T, int G,
+                                                     int64_t total_groups, int M,
+                                                     int32_t* __restrict__ lo_scr,
+                                                     int32_t* __restrict__ hi_scr,
+                                                     int32_t* __restrict__ tile_ptr) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t hist[NW][256];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_k;
+  __shared__ int64_t red;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t total = (int64_t)T * G;
+  uint64_t prefix = 0, pmask = 0;
+  int64_t k = total_groups;  // 1-based rank among candidates
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < NW * 256; i += NT) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < total; i += NT) {
+      const uint64_t d = gain_key(gains[i]);
+      const bool cand = (d & pmask) == prefix;
+      const uint32_t bin = (uint32_t)(d >> shift) & 255u;
+      const uint32_t act = __ballot_sync(0xffffffffu, cand);
+      if (cand) {
+        const uint32_t peers = __match_any_sync(act, bin);
+        if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[warp][bin], (uint32_t)__popc(peers));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // totals per bin (8 bins per lane), then the bin holding rank k
+      uint32_t c[8];
+      uint32_t sum = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        uint32_t v = 0;
+        for (int w = 0; w < NW; ++w) v += hist[w][lane * 8 + b];
+        c[b] = v;
+        sum += v;
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - sum;
+      const bool mine = (int64_t)excl < k && k <= (int64_t)incl;
+      const uint32_t who = __ballot_sync(0xffffffffu, mine);
+      if (lane == __ffs(who) - 1) {
+        int64_t before = excl;
+        int b = 0;
+        while (before + c[b] < k) { before += c[b]; ++b; }
+        s_prefix = prefix | ((uint64_t)(lane * 8 + b) << shift);
+        s_k = k - before;
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    k = s_k;
+    pmask |= (uint64_t)255 << shift;
+    __syncthreads();
+  }
+  const uint64_t xs = prefix;  // the total_groups-th smallest key
+  int64_t less = 0;
+  for (int t = threadIdx.x; t < T; t += NT) {
+    const double* row = gains + (int64_t)t * G;
+    int a = row_bound(row, G, xs, false), b = row_bound(row, G, xs, true);
+    lo_scr[t] = a;
+    hi_scr[t] = b;
+    less += a;
+  }
+  __syncthreads();
+  less = block_sum64<NT>(less, &red);
+  const int64_t R = total_groups - less;
+  int qlo = 0, qhi = G - 1;
+  while (qlo < qhi) {
+    int mid = (qlo + qhi) >> 1;
+    int64_t f = 0;
+    for (int t = threadIdx.x; t < T; t += NT) {
+      int v = min(hi_scr[t], mid + 1) - lo_scr[t];
+      f += v > 0 ? v : 0;
+    }
+    f = block_sum64<NT>(f, &red);
+    if (f >= R) qhi = mid; else qlo = mid + 1;
+  }
+  const int Q = qlo;
+  int64_t below = 0;
+  for (int t = threadIdx.x; t < T; t += NT) {
+    int v = min(hi_scr[t], Q) - lo_scr[t];
+    below += v > 0 ? v : 0;
+  }
+  below = block_sum64<NT>(below, &red);
+  const int64_t rem = R - below;
+  typedef cub::BlockScan<int64_t, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ int64_t carry_at, carry_ptr;
+  if (threadIdx.x == 0) { carry_at = 0; carry_ptr = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += NT) {
+    int t = base + threadIdx.x;
+    int64_t at_q = 0, cnt = 0;
+    if (t < T) {
+      int l = lo_scr[t], h = hi_scr[t];
+      int v = min(h, Q) - l;
+      cnt = l + (v > 0 ? v : 0);
+      at_q = (l <= Q && Q < h) ? 1 : 0;
+    }
+    int64_t excl_at;
+    BS(scan_tmp).ExclusiveSum(at_q, excl_at);
+    __syncthreads();
+    if (at_q && carry_at + excl_at < rem) cnt += 1;
+    int64_t cols = cnt * M, excl_cols;
+    BS(scan_tmp).ExclusiveSum(cols, excl_cols);
+    __syncthreads();
+    if (t < T) tile_ptr[t] = (int32_t)(carry_ptr + excl_cols);
+    int64_t tot_at = block_sum64<NT>(at_q, &red);
+    int64_t tot_cols = block_sum64<NT>(cols, &red);
+    if (threadIdx.x == 0) { carry_at += tot_at; carry_ptr += tot_cols; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
+}
+
 // a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_survivors(const int32_t* __restrict__ order, int n,
@@ -349,6 +506,62 @@ __global__ void k_nm_select(int mode, Src src, const uint8_t* __restrict__ em_in
   }
 }
 
+// a8/a10 fast path for the fused compressor (scores = |W| from bf16): one CTA per (tile, R rows).
+// sigma_i[t] and each W row are staged in shared memory with coalesced loads, so W is read
+// once from HBM instead of as scattered 2-byte gathers.
+template <int NT, int R>
+__global__ void __launch_bounds__(NT) k_nm_select_rows(const uint16_t* __restrict__ W, int64_t ldw,
+                                                       const int32_t* __restrict__ sigma_o,
+                                                       const int32_t* __restrict__ sig_ptr,
+                                                       const int32_t* __restrict__ sig_idx, int n,
+                                                       int V, int N, int M,
+                                                       uint8_t* __restrict__ nm_pos,
+                                                       uint16_t* __restrict__ kept) {
+  extern __shared__ __align__(16) uint8_t rows_smem[];
+  int32_t* s_idx = reinterpret_cast<int32_t*>(rows_smem);
+  uint16_t* s_row = reinterpret_cast<uint16_t*>(rows_smem + (((size_t)n * 4 + 15) & ~size_t(15)));
+  const int t = blockIdx.y;
+  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b;
+  const int G = k / M;
+  if (G == 0) return;
+  for (int i = threadIdx.x; i < k; i += NT) s_idx[i] = sig_idx[b + i];
+  const int64_t out_base = (int64_t)V * (b / M) * N;
+  for (int rr = 0; rr < R; ++rr) {
+    const int r = blockIdx.x * R + rr;
+    if (r >= V) break;
+    const uint16_t* wrow = W + (int64_t)sigma_o[(int64_t)t * V + r] * ldw;
+    __syncthreads();  // previous row fully consumed
+    if ((ldw & 7) == 0 && (n & 7) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(wrow);
+      uint4* dst = reinterpret_cast<uint4*>(s_row);
+      for (int i = threadIdx.x; i < n / 8; i += NT) dst[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < n; i += NT) s_row[i] = wrow[i];
+    }
+    __syncthreads();
+    const int64_t rbase = out_base + (int64_t)r * G * N;
+    for (int g = threadIdx.x; g < G; g += NT) {
+      const int32_t* cols = s_idx + g * M;
+      uint16_t v[32];
+      double sc[32];
+      for (int i = 0; i < M; ++i) {
+        v[i] = s_row[cols[i]];
+        sc[i] = bf16_abs_f64(v[i]);
+      }
+      int ns = 0;
+      for (int i = 0; i < M; ++i) {
+        int rank = 0;
+        for (int q = 0; q < M; ++q) rank += (sc[q] > sc[i]) || (sc[q] == sc[i] && q < i);
+        if (rank < N) {
+          nm_pos[rbase + (int64_t)g * N + ns] = (uint8_t)i;
+          kept[rbase + (int64_t)g * N + ns] = v[i];
+          ++ns;
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Operand image for the tcgen05 SpMM (see spmm_sm100.cu for the consumer side).
 //   kp_t = round_up(k_t, 64); a stage covers 64 logical K = 32 compressed values per row.
@@ -488,6 +701,29 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   return HINM_OK;
 }
 
+template <int ITEMS>
+int launch_tile_sort_items(const double* scores, int n, int T, double* sorted, int32_t* order,
+                           cudaStream_t stream) {
+  typedef cub::BlockRadixSort<double, 1024, ITEMS, int32_t> BRS;
+  const size_t smem = sizeof(typename BRS::TempStorage);
+  if (smem > 48 * 1024)
+    HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<1024, ITEMS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tile_sort<1024, ITEMS><<<T, 1024, smem, stream>>>(scores, n, sorted, order);
+  HINM_LAUNCH_CHECK();
+  return HINM_OK;
+}
+
+int launch_tile_sort(const double* scores, int n, int T, double* sorted, int32_t* order,
+                     cudaStream_t stream) {
+  if (n <= 1024) return launch_tile_sort_items<1>(scores, n, T, sorted, order, stream);
+  if (n <= 2048) return launch_tile_sort_items<2>(scores, n, T, sorted, order, stream);
+  if (n <= 4096) return launch_tile_sort_items<4>(scores, n, T, sorted, order, stream);
+  if (n <= 8192) return launch_tile_sort_items<8>(scores, n, T, sorted, order, stream);
+  if (n <= 12288) return launch_tile_sort_items<12>(scores, n, T, sorted, order, stream);
+  return launch_tile_sort_items<16>(scores, n, T, sorted, order, stream);
+}
+
 int status_from_rank(int code, int mask_mode) {
   if (code == INT_MAX) return HINM_OK;
   int rank = code % 16;
@@ -551,15 +787,21 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
   k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
   HINM_LAUNCH_CHECK();
-  size_t cb = workspace_bytes - L.cub;
-  HINM_CUDA_TRY(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-      ws + L.cub, cb, scores, sorted, vals_in, order, Tn, T, offsets, offsets + 1, 0, 64, stream));
+  if (n <= 16384) {
+    // one CTA per tile, stable block radix sort (descending)
+    int st2 = launch_tile_sort(scores, n, T, sorted, order, stream);
+    if (st2) return st2;
+  } else {
+    size_t cb = workspace_bytes - L.cub;
+    HINM_CUDA_TRY(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+        ws + L.cub, cb, scores, sorted, vals_in, order, Tn, T, offsets, offsets + 1, 0, 64, stream));
+  }
   if (G > 0) {
     k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains);
     HINM_LAUNCH_CHECK();
   }
-  k_budget<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, (int32_t*)(ws + L.lo),
-                                         (int32_t*)(ws + L.hi), tile_ptr);
+  k_budget_radix<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, (int32_t*)(ws + L.lo),
+                                               (int32_t*)(ws + L.hi), tile_ptr);
   HINM_LAUNCH_CHECK();
   const size_t smem = (size_t)n;
   if (smem > 48 * 1024)
@@ -629,7 +871,7 @@ extern "C" int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const do
     status = HINM_ERR_CUDA;
     goto done;
   }
-  if (K / M > 0) {
+  if (K / M > 0 && (element_mask_out || nm_pos || kept_bf16 || kept_f64 || mask_mode)) {
     const int64_t groups = K / M;
     Src src{W, ldw, Wd, ldwd, S, lds};
     k_nm_select<<<(unsigned)ceil_div(groups * V, 256), 256, 0, stream>>>(
@@ -692,10 +934,25 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t*
   if (st) return st;
   const int32_t* sp = own_sigma ? tptr : sig_ptr;
   const int32_t* si = own_sigma ? surv : sig_idx;
-  st = hinm_nm_select(HINM_SELECT_SCORES, W, ldw, nullptr, 0, nullptr, 0, nullptr, sigma_o, vmask,
-                      sp, si, p->m, p->n, p->V, p->N, p->M, -1, nullptr, p->nm_pos, p->kept_bf16,
-                      nullptr, stream_);
-  if (st) return st;
+  const size_t rsmem = (((size_t)p->n * 4 + 15) & ~size_t(15)) + (size_t)p->n * 2;
+  const bool fast = rsmem <= 200 * 1024 && p->M <= 32 && p->N <= 16;
+  if (!own_sigma || !fast) {
+    // validates a caller-supplied sigma_i (and selects when the fast path does not apply)
+    st = hinm_nm_select(HINM_SELECT_SCORES, W, ldw, nullptr, 0, nullptr, 0, nullptr, sigma_o, vmask,
+                        sp, si, p->m, p->n, p->V, p->N, p->M, -1, nullptr,
+                        fast ? nullptr : p->nm_pos, fast ? nullptr : p->kept_bf16, nullptr, stream_);
+    if (st) return st;
+  }
+  if (fast) {
+    constexpr int R = 4;
+    if (rsmem > 48 * 1024)
+      HINM_CUDA_TRY(cudaFuncSetAttribute(k_nm_select_rows<256, R>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+    dim3 grid((unsigned)ceil_div(p->V, R), p->T);
+    k_nm_select_rows<256, R><<<grid, 256, rsmem, stream>>>(W, ldw, sigma_o, sp, si, p->n, p->V, p->N,
+                                                           p->M, p->nm_pos, p->kept_bf16);
+    HINM_LAUNCH_CHECK();
+  }
   if (!own_sigma)
     HINM_CUDA_TRY(cudaMemcpyAsync(p->vec_idx, sig_idx, (size_t)p->total_keep * 4,
                                   cudaMemcpyDeviceToDevice, stream));

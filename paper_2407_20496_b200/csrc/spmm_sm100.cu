@@ -240,7 +240,9 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
   return q;
 }
 
-template <int MODE, int GW>
+// DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
+// 2 = skip the gather (measure the MMA pipeline alone).  Results are garbage when DBG != 0.
+template <int MODE, int GW, int DBG = 0>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
                 int64_t ldx, Params p) {
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
             const int row = __shfl_sync(0xffffffffu, my_row, i);
-            cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
+            if (DBG != 2) cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
           }
           cp_async_arrive_noinc(bar_full + 8 * stage);
         } else {
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
             const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2 + j;
             const uint64_t a_desc = smem_desc(sA + stage * V * 64 + j * 32 * V, 128, 256, 0);
             const uint64_t b_desc = smem_desc(sB + stage * B_STAGE + j * 4096, B_STAGE / 4, 1024, 2);
-            mma_sp(tmem, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
+            if (DBG != 1) mma_sp(tmem, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
           }
           tc_commit(bar_empty + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -582,6 +584,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "cp8")) return 1;
     if (!strcmp(e, "tma") || !strcmp(e, "tma2")) return 2;
     if (!strcmp(e, "tma4")) return 3;
+    if (!strcmp(e, "dbg_nomma")) return 4;
+    if (!strcmp(e, "dbg_nogather")) return 5;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
@@ -595,6 +599,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 1: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
     case 2: rc = launch(k_hinm_spmm<GATHER_TMA, 2>, 2); break;
     case 3: rc = launch(k_hinm_spmm<GATHER_TMA, 4>, 4); break;
+    case 4: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 1>, 8); break;
+    case 5: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 2>, 8); break;
     default: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
   }
   if (rc) return rc;
