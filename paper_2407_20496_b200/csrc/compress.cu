@@ -244,9 +244,10 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < NW * 256; i += NT) (&hist[0][0])[i] = 0;
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < total; i += NT) {
-      const uint64_t d = gain_key(gains[i]);
-      const bool cand = (d & pmask) == prefix;
+    for (int64_t i0 = 0; i0 < total; i0 += NT) {  // warp-uniform trip count (ballot below)
+      const int64_t i = i0 + threadIdx.x;
+      const uint64_t d = i < total ? gain_key(gains[i]) : 0;
+      const bool cand = i < total && (d & pmask) == prefix;
       const uint32_t bin = (uint32_t)(d >> shift) & 255u;
       const uint32_t act = __ballot_sync(0xffffffffu, cand);
       if (cand) {
