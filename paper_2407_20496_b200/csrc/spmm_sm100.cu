@@ -64,7 +64,7 @@ __host__ __device__ inline SmemLayout smem_layout(int V) {
   L.a = STAGES * B_STAGE;
   L.e = L.a + STAGES * V * 64 + 4096;          // 4 KB slack: M=128 descriptor over-read
   L.bar = L.e + STAGES * E_STAGE;
-  L.tmem = L.bar + (2 * STAGES + 2) * 8;
+  L.tmem = L.bar + (2 * STAGES + 4) * 8;
   L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
   return L;
 }
@@ -242,7 +242,11 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 
 // DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
 // 2 = skip the gather (measure the MMA pipeline alone).  Results are garbage when DBG != 0.
-template <int MODE, int GW, int DBG = 0>
+// M64: V <= 64 on the M=64 instruction.  Its accumulator occupies TMEM lanes 32q+0..15, so two
+// accumulators (lane offset 0 / 16) share the 256 columns: the epilogue of unit i overlaps the
+// mainloop of unit i+1.  Metadata for M=64 row 16q+l sits where M=128 row 32q+l would
+// (TMEM lanes 32q+0..15), measured with scripts/probe_sparse_meta.cu.
+template <int MODE, int GW, int DBG = 0, bool M64 = false>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
                 int64_t ldx, Params p) {
@@ -256,14 +260,22 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
   const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
-  const uint32_t bar_acc_full = bar_empty + STAGES * 8, bar_acc_empty = bar_acc_full + 8;
+  constexpr int NACC = M64 ? 2 : 1;  // accumulator buffers
+  const uint32_t bar_acc_full = bar_empty + STAGES * 8;   // [NACC]
+  const uint32_t bar_acc_empty = bar_acc_full + 16;       // [NACC]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
-  const int n_epi_warps = V >= 128 ? 4 : V / 32;  // quadrants that hold real rows
+  // warps (= TMEM lane quadrants) that hold real rows
+  const int n_epi_warps = M64 ? V / 16 : (V >= 128 ? 4 : V / 32);
 
-  // constant metadata for rows >= V in every E slot (never overwritten by the producer)
-  for (int i = threadIdx.x; i < STAGES * (128 - V) * 4; i += NT) {
-    const int s = i / ((128 - V) * 4), w = i % ((128 - V) * 4);
-    reinterpret_cast<uint32_t*>(gbase + L.e + s * E_STAGE + V * 16)[w] = META_PAD;
+  // constant metadata for lanes the producer never writes (rows >= V, M=64 gap lanes)
+  if (M64) {
+    for (int i = threadIdx.x; i < STAGES * E_STAGE / 4; i += NT)
+      reinterpret_cast<uint32_t*>(gbase + L.e)[i] = META_PAD;
+  } else {
+    for (int i = threadIdx.x; i < STAGES * (128 - V) * 4; i += NT) {
+      const int s = i / ((128 - V) * 4), w = i % ((128 - V) * 4);
+      reinterpret_cast<uint32_t*>(gbase + L.e + s * E_STAGE + V * 16)[w] = META_PAD;
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -271,8 +283,10 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       mbar_init(bar_full + 8 * s, MODE == GATHER_CPASYNC ? 1 + 32 * GW : 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
-    mbar_init(bar_acc_full, 1);
-    mbar_init(bar_acc_empty, n_epi_warps);
+    for (int a = 0; a < NACC; ++a) {
+      mbar_init(bar_acc_full + 8 * a, 1);
+      mbar_init(bar_acc_empty + 8 * a, n_epi_warps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (MODE == GATHER_TMA) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
   }
@@ -305,8 +319,15 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const uint32_t a_bytes = V * 64, e_bytes = (s & 1) ? 0 : V * 16;
           mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
           bulk_g2s(sA + stage * V * 64, p.a_vals + (int64_t)(k0 + s * BK) * V / 2, a_bytes, fb);
-          if (e_bytes)
-            bulk_g2s(sE + stage * E_STAGE, p.a_meta + ((int64_t)e0 + s / 2) * V * 4, e_bytes, fb);
+          if (e_bytes) {
+            const uint32_t* esrc = p.a_meta + ((int64_t)e0 + s / 2) * V * 4;
+            if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
+              for (int q = 0; q < V / 16; ++q)
+                bulk_g2s(sE + stage * E_STAGE + q * 512, esrc + q * 64, 256, fb);
+            } else {
+              bulk_g2s(sE + stage * E_STAGE, esrc, e_bytes, fb);
+            }
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -405,16 +426,19 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   } else if (warp == MMA_WARP) {
     // ============================================================ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = make_idesc(128, BN);
+      const uint32_t idesc = make_idesc(M64 ? 64 : 128, BN);
       int stage = 0;
-      uint32_t phase = 0, acc_phase = 0, eslot = 0;
+      uint32_t phase = 0, eslot = 0, ucount = 0;
       UnitParams nxt = unit_params(p, blockIdx.x);
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int kp = nxt.kp;
         nxt = unit_params(p, u + gridDim.x);
         if (kp == 0) continue;
-        mbar_wait(bar_acc_empty, acc_phase ^ 1);
+        const uint32_t acc = ucount % NACC, use = ucount / NACC;
+        ++ucount;
+        mbar_wait(bar_acc_empty + 8 * acc, (use & 1) ^ 1);
         tc_fence_after();
+        const uint32_t tmem_d = tmem + ((acc * 16u) << 16);
         for (int s = 0; s < kp / BK; ++s) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
@@ -428,13 +452,12 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
             const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2 + j;
             const uint64_t a_desc = smem_desc(sA + stage * V * 64 + j * 32 * V, 128, 256, 0);
             const uint64_t b_desc = smem_desc(sB + stage * B_STAGE + j * 4096, B_STAGE / 4, 1024, 2);
-            if (DBG != 1) mma_sp(tmem, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
+            if (DBG != 1) mma_sp(tmem_d, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
           }
           tc_commit(bar_empty + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(bar_acc_full);
-        acc_phase ^= 1;
+        tc_commit(bar_acc_full + 8 * acc);
       }
     }
     __syncwarp();
@@ -442,8 +465,10 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     // ============================================================ epilogue (warps 0-3)
     const int q = warp;  // TMEM lane quadrant of this warp
     if (q < n_epi_warps) {
-      uint32_t acc_phase = 0;
-      const int r = q * 32 + lane;
+      uint32_t ucount = 0;
+      // row of this thread: M=128 -> lane; M=64 -> lanes 0-15 (acc 0) and 16-31 (acc 1) both
+      // map to rows 16q + 0..15
+      const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
       auto out_row = [&](const UnitParams& q) -> int64_t {
         const int64_t prow = (int64_t)q.t * V + r;
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
@@ -459,12 +484,16 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         uint16_t* yrow = p.Y + orow * p.ldy;
         const int col_base = nb * BN;
         if (kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
+          if (M64 && lane >= 16) continue;
           for (int c = 0; c < BN; c += 8)
             if (col_base + c < p.B)
               *reinterpret_cast<uint4*>(yrow + col_base + c) = make_uint4(0, 0, 0, 0);
           continue;
         }
-        mbar_wait(bar_acc_full, acc_phase);
+        const uint32_t acc = ucount % NACC, use = ucount / NACC;
+        ++ucount;
+        const bool mine = !M64 || (uint32_t)(lane >> 4) == acc;
+        mbar_wait(bar_acc_full + 8 * acc, use & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -473,7 +502,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const int col = col_base + c * 32;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            if (col + h * 8 < p.B) {
+            if (mine && col + h * 8 < p.B) {
               uint4 o;
               o.x = pack_bf16x2(v[h * 8 + 0], v[h * 8 + 1]);
               o.y = pack_bf16x2(v[h * 8 + 2], v[h * 8 + 3]);
@@ -485,8 +514,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_acc_empty);
-        acc_phase ^= 1;
+        if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
       }
     }
   }
@@ -586,6 +614,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "tma4")) return 3;
     if (!strcmp(e, "dbg_nomma")) return 4;
     if (!strcmp(e, "dbg_nogather")) return 5;
+    if (!strcmp(e, "m128")) return 6;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
@@ -601,7 +630,11 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 3: rc = launch(k_hinm_spmm<GATHER_TMA, 4>, 4); break;
     case 4: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 1>, 8); break;
     case 5: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 2>, 8); break;
-    default: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
+    case 6: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8); break;  // M=128 for any V
+    default:
+      rc = pk->V <= 64 ? launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true>, 8)
+                       : launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8);
+      break;
   }
   if (rc) return rc;
   HINM_LAUNCH_CHECK();
