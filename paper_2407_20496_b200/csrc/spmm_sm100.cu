@@ -317,6 +317,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t fb = bar_full + 8 * stage;
           const uint32_t a_bytes = V * 64, e_bytes = (s & 1) ? 0 : V * 16;
+          if (DBG == 3) {  // experiment: no operand loads at all
+            mbar_arrive(fb);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
           bulk_g2s(sA + stage * V * 64, p.a_vals + (int64_t)(k0 + s * BK) * V / 2, a_bytes, fb);
           if (e_bytes) {
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
             const int row = __shfl_sync(0xffffffffu, my_row, i);
-            if (DBG != 2) cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
+            if (DBG != 2 && DBG != 3) cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
           }
           cp_async_arrive_noinc(bar_full + 8 * stage);
         } else {
@@ -615,6 +620,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_nomma")) return 4;
     if (!strcmp(e, "dbg_nogather")) return 5;
     if (!strcmp(e, "m128")) return 6;
+    if (!strcmp(e, "dbg_noload")) return 7;
+    if (!strcmp(e, "dbg_noload128")) return 8;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
@@ -631,6 +638,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 4: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 1>, 8); break;
     case 5: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 2>, 8); break;
     case 6: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8); break;  // M=128 for any V
+    case 7: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, true>, 8); break;
+    case 8: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, false>, 8); break;
     default:
       rc = pk->V <= 64 ? launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true>, 8)
                        : launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8);

@@ -27,7 +27,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 __constant__ uint32_t PAT[6] = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE};
 
 // out: [M][64] floats for each run
-__global__ void probe(int M, int run, int id2, float* out) {
+__global__ void probe(int M, int run, int id2, int dlane, int elane, int ecol0, float* out) {
   __shared__ __align__(1024) uint8_t sB[4096];
   __shared__ __align__(1024) uint8_t sA[4096];
   __shared__ uint64_t bar;
@@ -60,7 +60,7 @@ __global__ void probe(int M, int run, int id2, float* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  const uint32_t ECOL = 256;
+  const uint32_t ECOL = ecol0;
   // metadata: columns ECOL .. ECOL+3, every lane; slot id = (L * 8 + j) + 1024 * col
   {
     const int L = warp * 32 + lane;
@@ -73,6 +73,7 @@ __global__ void probe(int M, int run, int id2, float* out) {
         w |= PAT[d % 6] << (4 * j);
       }
       uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + ECOL + c;
+      if (((lane >> 4) << 4) != elane && elane != 0) w = 0x44444444u;  // only lanes 16-31 carry the pattern
       asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(w));
     }
     asm volatile("tcgen05.wait::st.sync.aligned;");
@@ -85,10 +86,10 @@ __global__ void probe(int M, int run, int id2, float* out) {
                            ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(M >> 4) << 24) | (uint32_t)id2;
     const uint64_t ad = desc(smem_u32(sA), 128, 256, 0);
     const uint64_t bd = desc(smem_u32(sB), 8192, 1024, 2);
-    const uint32_t te = tmem + ECOL;
+    const uint32_t te = tmem + ((uint32_t)elane << 16) + ECOL;
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
-        "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p;\n\t}\n" ::"r"(tmem),
+        "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p;\n\t}\n" ::"r"(tmem + ((uint32_t)dlane << 16)),
         "l"(ad), "l"(bd), "r"(te), "r"(idesc));
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
   }
@@ -118,51 +119,55 @@ int main() {
   cudaMalloc(&d, 128 * 64 * 4);
   static float h[4][128 * 64];
   const int pats[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-  for (int M : {128, 64}) {
-    for (int id2 = 0; id2 < 2; ++id2) {
-      for (int run = 0; run < 4; ++run) {
-        cudaMemset(d, 0, 128 * 64 * 4);
-        probe<<<1, 128>>>(M, run, id2, d);
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { printf("M=%d id2=%d run=%d error %s\n", M, id2, run, cudaGetErrorString(e)); return 1; }
-        cudaMemcpy(h[run], d, 128 * 64 * 4, cudaMemcpyDeviceToHost);
+  struct Cfg { int M, id2, dlane, elane, ecol; } cfgs[] = {
+      {64, 0, 0, 0, 256}, {64, 0, 16, 0, 256}, {64, 0, 0, 16, 256}, {64, 0, 16, 16, 256},
+      {64, 0, 0, 16, 0}};
+  for (auto cf : cfgs) {
+    bool bad = false;
+    for (int run = 0; run < 4; ++run) {
+      cudaMemset(d, 0, 128 * 64 * 4);
+      probe<<<1, 128>>>(cf.M, run, cf.id2, cf.dlane, cf.elane, cf.ecol, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("M=%d dlane=%d elane=%d ecol=%d: error %s\n", cf.M, cf.dlane, cf.elane, cf.ecol, cudaGetErrorString(e));
+        return 0;  // context is dead after an error
       }
-      printf("=== M=%d id2=%d : (D lane, chunk) -> metadata slot (col, lane, nibble)\n", M, id2);
-      for (int L = 0; L < 128; ++L) {
-        // which chunks of this D lane carry values?
-        char line[4096];
-        int pos = snprintf(line, sizeof line, "lane %3d:", L);
-        bool any = false;
-        for (int c = 0; c < 8; ++c) {
-          int slot = 0, mul = 1;
-          bool ok = true;
-          for (int run = 0; run < 4; ++run) {
-            const float* row = h[run] + L * 64;
-            // expected values 2c+1 and 2c+2 somewhere in [4c, 4c+4)
-            int p0 = -1, p1 = -1;
-            for (int q = 0; q < 4; ++q) {
-              float v = row[4 * c + q];
-              if (v == (float)(2 * c + 1)) p0 = q;
-              if (v == (float)(2 * c + 2)) p1 = q;
-            }
-            int pi = -1;
-            for (int k = 0; k < 6; ++k)
-              if (pats[k][0] == p0 && pats[k][1] == p1) pi = k;
-            if (pi < 0) { ok = false; break; }
-            slot += pi * mul;
-            mul *= 6;
+      cudaMemcpy(h[run], d, 128 * 64 * 4, cudaMemcpyDeviceToHost);
+    }
+    printf("=== M=%d id2=%d dlane=%d elane=%d ecol=%d\n", cf.M, cf.id2, cf.dlane, cf.elane, cf.ecol);
+    for (int L = 0; L < 128; ++L) {
+      char line[4096];
+      int pos = snprintf(line, sizeof line, "lane %3d:", L);
+      bool any = false;
+      for (int c = 0; c < 8; ++c) {
+        int slot = 0, mul = 1;
+        bool ok = true;
+        for (int run = 0; run < 4; ++run) {
+          const float* row = h[run] + L * 64;
+          int p0 = -1, p1 = -1;
+          for (int q = 0; q < 4; ++q) {
+            float v = row[4 * c + q];
+            if (v == (float)(2 * c + 1)) p0 = q;
+            if (v == (float)(2 * c + 2)) p1 = q;
           }
-          if (ok) {
-            any = true;
-            pos += snprintf(line + pos, sizeof line - pos, " c%d->(col%d,L%d,n%d)", c, slot / 1024,
-                            (slot % 1024) / 8, slot % 8);
-          } else {
-            pos += snprintf(line + pos, sizeof line - pos, " c%d->?", c);
-          }
+          int pi = -1;
+          for (int k = 0; k < 6; ++k)
+            if (pats[k][0] == p0 && pats[k][1] == p1) pi = k;
+          if (pi < 0) { ok = false; break; }
+          slot += pi * mul;
+          mul *= 6;
         }
-        if (any) printf("%s\n", line);
+        if (ok) {
+          any = true;
+          pos += snprintf(line + pos, sizeof line - pos, " c%d->(col%d,L%d,n%d)", c, slot / 1024,
+                          (slot % 1024) / 8, slot % 8);
+        } else {
+          pos += snprintf(line + pos, sizeof line - pos, " c%d->?", c);
+        }
       }
+      if (any && (L % 16 == 0 || L % 16 == 8)) printf("%s\n", line);
     }
   }
+  (void)bad;
   return 0;
 }
