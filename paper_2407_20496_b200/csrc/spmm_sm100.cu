@@ -242,10 +242,10 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 
 // DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
 // 2 = skip the gather (measure the MMA pipeline alone).  Results are garbage when DBG != 0.
-// M64: V <= 64 on the M=64 instruction.  Its accumulator occupies TMEM lanes 32q+0..15, so two
-// accumulators (lane offset 0 / 16) share the 256 columns: the epilogue of unit i overlaps the
-// mainloop of unit i+1.  Metadata for M=64 row 16q+l sits where M=128 row 32q+l would
-// (TMEM lanes 32q+0..15), measured with scripts/probe_sparse_meta.cu.
+// M64: V <= 64 on the M=64 instruction (half the A-operand shared-memory reads of M=128).  Its
+// accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
+// (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
+// M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
 template <int MODE, int GW, int DBG = 0, bool M64 = false>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
   const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
-  constexpr int NACC = M64 ? 2 : 1;  // accumulator buffers
+  constexpr int NACC = 1;  // accumulator buffers
   const uint32_t bar_acc_full = bar_empty + STAGES * 8;   // [NACC]
   const uint32_t bar_acc_empty = bar_acc_full + 16;       // [NACC]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
@@ -471,8 +471,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     const int q = warp;  // TMEM lane quadrant of this warp
     if (q < n_epi_warps) {
       uint32_t ucount = 0;
-      // row of this thread: M=128 -> lane; M=64 -> lanes 0-15 (acc 0) and 16-31 (acc 1) both
-      // map to rows 16q + 0..15
+      // row of this thread: M=128 -> lane; M=64 -> lanes 0-15 hold rows 16q + 0..15
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
       auto out_row = [&](const UnitParams& q) -> int64_t {
         const int64_t prow = (int64_t)q.t * V + r;
@@ -497,7 +496,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         }
         const uint32_t acc = ucount % NACC, use = ucount / NACC;
         ++ucount;
-        const bool mine = !M64 || (uint32_t)(lane >> 4) == acc;
+        const bool mine = !M64 || lane < 16;
         mbar_wait(bar_acc_full + 8 * acc, use & 1);
         tc_fence_after();
 #pragma unroll 1
