@@ -12,6 +12,7 @@
 //   k_nm_select   a8/a10 top-N per sigma_i group, reference view (nm_index, kept_values)
 //   k_pack_*      a10  operand image for the tcgen05 SpMM (padded gather index, UMMA A, E)
 #include <climits>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -50,6 +51,58 @@ __global__ void k_scores(Src src, const int32_t* __restrict__ sigma_o, int n, in
     for (int r = 1; r < V; ++r) acc = acc + src.score(rows[r], j);
   }
   scores[(int64_t)t * n + j] = acc + 0.0;  // canonicalise -0.0 (only compared, never emitted)
+}
+
+// a3 (bf16 fast path, n % 8 == 0): 8 consecutive columns per thread (one 16-byte load per
+// row), independent fp64 chains per column, still summed sequentially in sigma_o row order.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, int64_t ldw,
+                                                const int32_t* __restrict__ sigma_o, int n, int V,
+                                                double* __restrict__ scores) {
+  extern __shared__ int32_t s_rows[];
+  const int t = blockIdx.y;
+  for (int r = threadIdx.x; r < V; r += NT) s_rows[r] = sigma_o[(int64_t)t * V + r];
+  __syncthreads();
+  const int j0 = (blockIdx.x * NT + threadIdx.x) * 8;
+  if (j0 >= n) return;
+  double acc[8];
+  {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[0] * ldw + j0));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc[2 * k] = bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
+      acc[2 * k + 1] = bf16_abs_f64((uint16_t)(w[k] >> 16));
+    }
+  }
+  int r = 1;
+  for (; r + 4 <= V; r += 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[r + u] * ldw + j0));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc[2 * k] = acc[2 * k] + bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
+        acc[2 * k + 1] = acc[2 * k + 1] + bf16_abs_f64((uint16_t)(w[k] >> 16));
+      }
+    }
+  }
+  for (; r < V; ++r) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[r] * ldw + j0));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc[2 * k] = acc[2 * k] + bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
+      acc[2 * k + 1] = acc[2 * k + 1] + bf16_abs_f64((uint16_t)(w[k] >> 16));
+    }
+  }
+  double* out = scores + (int64_t)t * n + j0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) out[k] = acc[k] + 0.0;
 }
 
 __global__ void k_iota_cols(int32_t* __restrict__ v, int n, int64_t total) {
@@ -200,7 +253,7 @@ template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_tile_sort(const double* __restrict__ scores, int n,
                                                   double* __restrict__ sorted,
                                                   int32_t* __restrict__ order) {
-  typedef cub::BlockRadixSort<double, NT, ITEMS, int32_t> BRS;
+  typedef cub::BlockRadixSort<double, NT, ITEMS, int32_t, 6> BRS;
   extern __shared__ __align__(16) uint8_t sort_smem[];
   typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(sort_smem);
   const int t = blockIdx.x;
@@ -222,6 +275,74 @@ __global__ void __launch_bounds__(NT) k_tile_sort(const double* __restrict__ sco
       order[(int64_t)t * n + j] = vals[i];
     }
   }
+}
+
+// Tail of the budget selection once the threshold key xs (the G-th smallest (-gain) key) is
+// known: per-tile counts with ties ordered by (q, t), written as the tile_ptr prefix.
+template <int NT>
+__device__ void budget_tail(const double* __restrict__ gains, int T, int G, int64_t total_groups,
+                            int M, uint64_t xs, bool compute_bounds, int32_t* __restrict__ lo_scr,
+                            int32_t* __restrict__ hi_scr, int32_t* __restrict__ tile_ptr) {
+  __shared__ int64_t red;
+  int64_t less = 0;
+  for (int t = threadIdx.x; t < T; t += NT) {
+    if (compute_bounds) {
+      const double* row = gains + (int64_t)t * G;
+      lo_scr[t] = row_bound(row, G, xs, false);
+      hi_scr[t] = row_bound(row, G, xs, true);
+    }
+    less += lo_scr[t];
+  }
+  __syncthreads();
+  less = block_sum64<NT>(less, &red);
+  const int64_t R = total_groups - less;
+  int qlo = 0, qhi = G - 1;
+  while (qlo < qhi) {
+    int mid = (qlo + qhi) >> 1;
+    int64_t f = 0;
+    for (int t = threadIdx.x; t < T; t += NT) {
+      int v = min(hi_scr[t], mid + 1) - lo_scr[t];
+      f += v > 0 ? v : 0;
+    }
+    f = block_sum64<NT>(f, &red);
+    if (f >= R) qhi = mid; else qlo = mid + 1;
+  }
+  const int Q = qlo;
+  int64_t below = 0;
+  for (int t = threadIdx.x; t < T; t += NT) {
+    int v = min(hi_scr[t], Q) - lo_scr[t];
+    below += v > 0 ? v : 0;
+  }
+  below = block_sum64<NT>(below, &red);
+  const int64_t rem = R - below;
+  typedef cub::BlockScan<int64_t, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ int64_t carry_at, carry_ptr;
+  if (threadIdx.x == 0) { carry_at = 0; carry_ptr = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += NT) {
+    int t = base + threadIdx.x;
+    int64_t at_q = 0, cnt = 0;
+    if (t < T) {
+      int l = lo_scr[t], h = hi_scr[t];
+      int v = min(h, Q) - l;
+      cnt = l + (v > 0 ? v : 0);
+      at_q = (l <= Q && Q < h) ? 1 : 0;
+    }
+    int64_t excl_at;
+    BS(scan_tmp).ExclusiveSum(at_q, excl_at);
+    __syncthreads();
+    if (at_q && carry_at + excl_at < rem) cnt += 1;
+    int64_t cols = cnt * M, excl_cols;
+    BS(scan_tmp).ExclusiveSum(cols, excl_cols);
+    __syncthreads();
+    if (t < T) tile_ptr[t] = (int32_t)(carry_ptr + excl_cols);
+    int64_t tot_at = block_sum64<NT>(at_q, &red);
+    int64_t tot_cols = block_sum64<NT>(cols, &red);
+    if (threadIdx.x == 0) { carry_at += tot_at; carry_ptr += tot_cols; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
 }
 
 // a5 (fast path): exact radix select of the G-th smallest key d = ~bits(gain) over all tiles
@@ -290,65 +411,90 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
     pmask |= (uint64_t)255 << shift;
     __syncthreads();
   }
-  const uint64_t xs = prefix;  // the total_groups-th smallest key
-  int64_t less = 0;
-  for (int t = threadIdx.x; t < T; t += NT) {
+  budget_tail<NT>(gains, T, G, total_groups, M, prefix, true, lo_scr, hi_scr, tile_ptr);
+}
+
+
+// a5, multi-CTA: the same radix select with the key histogram split over the whole grid
+// (cooperative launch, one grid-wide barrier per 8-bit digit).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ gains, int T, int G,
+                                                    int64_t total_groups, int M,
+                                                    uint32_t* __restrict__ ghist,
+                                                    int32_t* __restrict__ lo_scr,
+                                                    int32_t* __restrict__ hi_scr,
+                                                    int32_t* __restrict__ tile_ptr) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t hist[NW][256];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t total = (int64_t)T * G;
+  uint64_t prefix = 0, pmask = 0;
+  int64_t k = total_groups;
+  int pass = 0;
+  for (int shift = 56; shift >= 0; shift -= 8, ++pass) {
+    for (int i = threadIdx.x; i < NW * 256; i += NT) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
+      const int64_t i = i0 + threadIdx.x;
+      const uint64_t d = i < total ? gain_key(gains[i]) : 0;
+      const bool cand = i < total && (d & pmask) == prefix;
+      const uint32_t bin = (uint32_t)(d >> shift) & 255u;
+      const uint32_t act = __ballot_sync(0xffffffffu, cand);
+      if (cand) {
+        const uint32_t peers = __match_any_sync(act, bin);
+        if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[warp][bin], (uint32_t)__popc(peers));
+      }
+    }
+    __syncthreads();
+    for (int bn = threadIdx.x; bn < 256; bn += NT) {
+      uint32_t v = 0;
+      for (int w = 0; w < NW; ++w) v += hist[w][bn];
+      if (v) atomicAdd(ghist + pass * 256 + bn, v);
+    }
+    grid.sync();
+    if (warp == 0) {
+      uint32_t c[8];
+      uint32_t sum = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        c[b] = __ldcg(ghist + pass * 256 + lane * 8 + b);
+        sum += c[b];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - sum;
+      const bool mine = (int64_t)excl < k && k <= (int64_t)incl;
+      const uint32_t who = __ballot_sync(0xffffffffu, mine);
+      if (lane == __ffs(who) - 1) {
+        int64_t before = excl;
+        int b = 0;
+        while (before + c[b] < k) { before += c[b]; ++b; }
+        s_prefix = prefix | ((uint64_t)(lane * 8 + b) << shift);
+        s_k = k - before;
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    k = s_k;
+    pmask |= (uint64_t)255 << shift;
+    __syncthreads();
+  }
+  for (int t = blockIdx.x * NT + threadIdx.x; t < T; t += gridDim.x * NT) {
     const double* row = gains + (int64_t)t * G;
-    int a = row_bound(row, G, xs, false), b = row_bound(row, G, xs, true);
-    lo_scr[t] = a;
-    hi_scr[t] = b;
-    less += a;
+    lo_scr[t] = row_bound(row, G, prefix, false);
+    hi_scr[t] = row_bound(row, G, prefix, true);
   }
-  __syncthreads();
-  less = block_sum64<NT>(less, &red);
-  const int64_t R = total_groups - less;
-  int qlo = 0, qhi = G - 1;
-  while (qlo < qhi) {
-    int mid = (qlo + qhi) >> 1;
-    int64_t f = 0;
-    for (int t = threadIdx.x; t < T; t += NT) {
-      int v = min(hi_scr[t], mid + 1) - lo_scr[t];
-      f += v > 0 ? v : 0;
-    }
-    f = block_sum64<NT>(f, &red);
-    if (f >= R) qhi = mid; else qlo = mid + 1;
-  }
-  const int Q = qlo;
-  int64_t below = 0;
-  for (int t = threadIdx.x; t < T; t += NT) {
-    int v = min(hi_scr[t], Q) - lo_scr[t];
-    below += v > 0 ? v : 0;
-  }
-  below = block_sum64<NT>(below, &red);
-  const int64_t rem = R - below;
-  typedef cub::BlockScan<int64_t, NT> BS;
-  __shared__ typename BS::TempStorage scan_tmp;
-  __shared__ int64_t carry_at, carry_ptr;
-  if (threadIdx.x == 0) { carry_at = 0; carry_ptr = 0; }
-  __syncthreads();
-  for (int base = 0; base < T; base += NT) {
-    int t = base + threadIdx.x;
-    int64_t at_q = 0, cnt = 0;
-    if (t < T) {
-      int l = lo_scr[t], h = hi_scr[t];
-      int v = min(h, Q) - l;
-      cnt = l + (v > 0 ? v : 0);
-      at_q = (l <= Q && Q < h) ? 1 : 0;
-    }
-    int64_t excl_at;
-    BS(scan_tmp).ExclusiveSum(at_q, excl_at);
-    __syncthreads();
-    if (at_q && carry_at + excl_at < rem) cnt += 1;
-    int64_t cols = cnt * M, excl_cols;
-    BS(scan_tmp).ExclusiveSum(cols, excl_cols);
-    __syncthreads();
-    if (t < T) tile_ptr[t] = (int32_t)(carry_ptr + excl_cols);
-    int64_t tot_at = block_sum64<NT>(at_q, &red);
-    int64_t tot_cols = block_sum64<NT>(cols, &red);
-    if (threadIdx.x == 0) { carry_at += tot_at; carry_ptr += tot_cols; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
+  grid.sync();
+  if (blockIdx.x != 0) return;
+  budget_tail<NT>(gains, T, G, total_groups, M, prefix, false, lo_scr, hi_scr, tile_ptr);
 }
 
 // a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
@@ -525,7 +671,18 @@ __global__ void __launch_bounds__(NT) k_nm_select_rows(const uint16_t* __restric
   const int b = sig_ptr[t], k = sig_ptr[t + 1] - b;
   const int G = k / M;
   if (G == 0) return;
-  for (int i = threadIdx.x; i < k; i += NT) s_idx[i] = sig_idx[b + i];
+  {
+    int i = threadIdx.x;
+    for (; i + 3 * NT < k; i += 4 * NT) {  // 4 loads in flight per thread
+      const int32_t a0 = sig_idx[b + i], a1 = sig_idx[b + i + NT], a2 = sig_idx[b + i + 2 * NT],
+                    a3 = sig_idx[b + i + 3 * NT];
+      s_idx[i] = a0;
+      s_idx[i + NT] = a1;
+      s_idx[i + 2 * NT] = a2;
+      s_idx[i + 3 * NT] = a3;
+    }
+    for (; i < k; i += NT) s_idx[i] = sig_idx[b + i];
+  }
   const int64_t out_base = (int64_t)V * (b / M) * N;
   for (int rr = 0; rr < R; ++rr) {
     const int r = blockIdx.x * R + rr;
@@ -535,7 +692,17 @@ __global__ void __launch_bounds__(NT) k_nm_select_rows(const uint16_t* __restric
     if ((ldw & 7) == 0 && (n & 7) == 0) {
       const uint4* src = reinterpret_cast<const uint4*>(wrow);
       uint4* dst = reinterpret_cast<uint4*>(s_row);
-      for (int i = threadIdx.x; i < n / 8; i += NT) dst[i] = src[i];
+      const int nv = n / 8;
+      int i = threadIdx.x;
+      for (; i + 3 * NT < nv; i += 4 * NT) {
+        const uint4 a0 = __ldg(src + i), a1 = __ldg(src + i + NT), a2 = __ldg(src + i + 2 * NT),
+                    a3 = __ldg(src + i + 3 * NT);
+        dst[i] = a0;
+        dst[i + NT] = a1;
+        dst[i + 2 * NT] = a2;
+        dst[i + 3 * NT] = a3;
+      }
+      for (; i < nv; i += NT) dst[i] = __ldg(src + i);
     } else {
       for (int i = threadIdx.x; i < n; i += NT) s_row[i] = wrow[i];
     }
@@ -610,6 +777,32 @@ __global__ void k_pack_vals(const int32_t* __restrict__ tile_ptr, const int32_t*
   a_vals[aval_offset(ko, V, r, (int)(2 * g_in + 1))] = kept[src + 1];
 }
 
+// 2:4 fast path: one thread writes one 16-byte core-matrix row (8 compressed values = 4 groups
+// of one weight row), reading 16 contiguous bytes of the reference view.
+__global__ void k_pack_vals16(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ kofs,
+                              const uint16_t* __restrict__ kept, int V,
+                              uint16_t* __restrict__ a_vals) {
+  const int t = blockIdx.y;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c_in = gid / V;     // chunk of 4 groups within the tile
+  const int r = (int)(gid % V);
+  const int Gt = (tile_ptr[t + 1] - tile_ptr[t]) / 4;
+  const int g0 = (int)(c_in * 4);
+  if (g0 >= Gt) return;
+  const uint16_t* src = kept + (int64_t)V * (tile_ptr[t] / 4) * 2 + (int64_t)r * Gt * 2 + g0 * 2;
+  uint16_t v[8];
+  const int ng = min(4, Gt - g0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = (i < 2 * ng) ? src[i] : (uint16_t)0;
+  // 8 compressed values 2*g0 .. 2*g0+7 are one contiguous 16 B core-matrix row (kc % 8 == 0)
+  uint4 o;
+  o.x = v[0] | ((uint32_t)v[1] << 16);
+  o.y = v[2] | ((uint32_t)v[3] << 16);
+  o.z = v[4] | ((uint32_t)v[5] << 16);
+  o.w = v[6] | ((uint32_t)v[7] << 16);
+  *reinterpret_cast<uint4*>(a_vals + aval_offset(kofs[t], V, r, 2 * g0)) = o;
+}
+
 // One thread per (tile, 128-block, lane, word): composes the 8 nibbles of the word.
 __global__ void k_pack_meta(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ eofs,
                             const uint8_t* __restrict__ nm_pos, int V, int T,
@@ -662,7 +855,7 @@ namespace hinm {
 namespace {
 
 struct WsLayout {
-  size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, err, cub, total;
+  size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, err, ghist, cub, total;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -694,6 +887,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->hi = take(4 * T);
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
   L->err = take(16);
+  L->ghist = take(8 * 256 * 4);
   size_t cb = 0;
   int st = cub_sort_bytes((int)T, n, &cb);
   if (st) return st;
@@ -705,7 +899,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
 template <int ITEMS>
 int launch_tile_sort_items(const double* scores, int n, int T, double* sorted, int32_t* order,
                            cudaStream_t stream) {
-  typedef cub::BlockRadixSort<double, 1024, ITEMS, int32_t> BRS;
+  typedef cub::BlockRadixSort<double, 1024, ITEMS, int32_t, 6> BRS;
   const size_t smem = sizeof(typename BRS::TempStorage);
   if (smem > 48 * 1024)
     HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<1024, ITEMS>,
@@ -782,7 +976,12 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   double* gains = (double*)(ws + L.gains);
   Src src{W, ldw, Wd, ldwd, S, lds};
 
-  k_scores<<<dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream>>>(src, sigma_o, n, V, scores);
+  if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
+    k_scores8<128><<<dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream>>>(
+        W, ldw, sigma_o, n, V, scores);
+  } else {
+    k_scores<<<dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream>>>(src, sigma_o, n, V, scores);
+  }
   HINM_LAUNCH_CHECK();
   const int64_t Tn = (int64_t)T * n;
   k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
@@ -801,9 +1000,28 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains);
     HINM_LAUNCH_CHECK();
   }
-  k_budget_radix<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, (int32_t*)(ws + L.lo),
-                                               (int32_t*)(ws + L.hi), tile_ptr);
-  HINM_LAUNCH_CHECK();
+  {
+    uint32_t* ghist = (uint32_t*)(ws + L.ghist);
+    int32_t* lo_s = (int32_t*)(ws + L.lo);
+    int32_t* hi_s = (int32_t*)(ws + L.hi);
+    HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4, stream));
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_budget_coop<1024>, 1024, 0);
+    const int64_t total = (int64_t)T * G;
+    int nblk = (int)std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, ceil_div(total, 4096)));
+    if (per_sm < 1 || nblk < 2) {
+      k_budget_radix<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, lo_s, hi_s, tile_ptr);
+      HINM_LAUNCH_CHECK();
+    } else {
+      int Ti = T, Gi = G, Mi = M;
+      int64_t gr = groups;
+      void* args[] = {(void*)&gains, &Ti, &Gi, &gr, &Mi, &ghist, &lo_s, &hi_s, &tile_ptr};
+      HINM_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_budget_coop<1024>, dim3(nblk), dim3(1024),
+                                                args, 0, stream));
+    }
+  }
   const size_t smem = (size_t)n;
   if (smem > 48 * 1024)
     HINM_CUDA_TRY(cudaFuncSetAttribute(k_survivors<1024>,
@@ -902,8 +1120,9 @@ extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
   HINM_CUDA_TRY(cudaMemsetAsync(p->a_vals, 0, (size_t)acap * 2, stream));
   const int64_t groups = p->total_keep / 4;
   if (groups > 0) {
-    k_pack_vals<<<(unsigned)ceil_div(groups * V, 256), 256, 0, stream>>>(
-        p->tile_ptr, p->tile_kofs, p->kept_bf16, V, T, groups, p->a_vals);
+    // one thread per (chunk of 4 groups, row); a tile has at most ceil(n / 16) chunks
+    dim3 gv((unsigned)ceil_div(ceil_div(p->n, 16) * V, 256), T);
+    k_pack_vals16<<<gv, 256, 0, stream>>>(p->tile_ptr, p->tile_kofs, p->kept_bf16, V, p->a_vals);
     HINM_LAUNCH_CHECK();
   }
   // a tile has at most ceil(round_up(n, 64) / 128) metadata blocks
