@@ -19,9 +19,9 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 }
 
 // sparse: 0 dense kind::f16 (K=16), 1 sparse (K=32), 2 sparse with A in TMEM
-__global__ void bench(int M, int N, int sparse, int iters, unsigned long long* cycles) {
+__global__ void bench(int M, int N, int sparse, int iters, int extra, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2, bar3;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5;
   uint8_t* sB = sm;             // 64 KB: K=32 rows x 256 tokens, SW128 MN-major
@@ -29,6 +29,9 @@ __global__ void bench(int M, int N, int sparse, int iters, unsigned long long* c
   for (int i = threadIdx.x; i < (65536 + 8192) / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0x3c003c00u;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(smem_u32(&bar2)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar3)));
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar3)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -73,6 +76,17 @@ __global__ void bench(int M, int N, int sparse, int iters, unsigned long long* c
                      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;\n\t}\n" ::"r"(tmem),
                      "r"(tmem + 256), "l"(bd), "r"(idesc), "r"(i), "r"(te));
       }
+      if ((extra & 1) && (i & 1))
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar2)));
+      if ((extra & 2) && (i & 3) == 3)
+        asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(tmem + 392), "l"(desc(smem_u32(sA), 0, 128, 0)));
+      if ((extra & 4) && (i & 1)) {
+        uint32_t dn = 0;
+        while (!dn)
+          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                       : "=r"(dn) : "r"(smem_u32(&bar3)));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     uint32_t done = 0;
@@ -94,31 +108,31 @@ int main() {
   cudaMalloc(&d, sms * 8);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 8192);
   const int iters = 4096;
-  printf("kind,M,N,K_logical,cycles_per_mma,ms,chip_TFLOPs_logical\n");
-  for (int sparse = 0; sparse < 3; ++sparse)
-    for (int M : {64, 128})
-      for (int N : {64, 128, 256}) {
-        if (sparse == 2 && M == 64) continue;
-        cudaEvent_t a, b;
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
-        bench<<<sms, 128, 65536 + 8192>>>(M, N, sparse, 64, d);  // warm
-        cudaEventRecord(a);
-        bench<<<sms, 128, 65536 + 8192>>>(M, N, sparse, iters, d);
-        cudaEventRecord(b);
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { printf("error %s (sparse=%d M=%d N=%d)\n", cudaGetErrorString(e), sparse, M, N); return 1; }
-        float ms;
-        cudaEventElapsedTime(&ms, a, b);
-        unsigned long long h[256];
-        cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
-        double avg = 0;
-        for (int i = 0; i < sms; ++i) avg += h[i];
-        avg /= sms;
-        const int K = sparse ? 32 : 16;
-        const double flops = 2.0 * M * N * K * (double)iters * sms;
-        printf("%s,%d,%d,%d,%.1f,%.3f,%.1f\n", sparse == 0 ? "dense" : (sparse == 1 ? "sparse_ss" : "sparse_ts"),
-               M, N, K, avg / iters, ms, flops / (ms * 1e-3) / 1e12);
-      }
+  printf("kind,M,N,K_logical,extra,cycles_per_mma,ms,chip_TFLOPs_logical\n");
+  struct C { int sparse, M, N, extra; } cs[] = {
+      {0, 128, 256, 0}, {1, 64, 256, 0}, {1, 128, 256, 0}, {2, 128, 256, 0}, {1, 64, 128, 0},
+      {1, 64, 256, 1}, {1, 64, 256, 3}, {1, 64, 256, 7}, {1, 128, 256, 7}, {1, 64, 128, 7}};
+  for (auto c : cs) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    bench<<<sms, 128, 65536 + 8192>>>(c.M, c.N, c.sparse, 64, c.extra, d);
+    cudaEventRecord(a);
+    bench<<<sms, 128, 65536 + 8192>>>(c.M, c.N, c.sparse, iters, c.extra, d);
+    cudaEventRecord(b);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    unsigned long long h[256];
+    cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < sms; ++i) avg += h[i];
+    avg /= sms;
+    const int K = c.sparse ? 32 : 16;
+    const double flops = 2.0 * c.M * c.N * K * (double)iters * sms;
+    printf("%s,%d,%d,%d,%d,%.1f,%.3f,%.1f\n", c.sparse == 0 ? "dense" : (c.sparse == 1 ? "sparse_ss" : "sparse_ts"),
+           c.M, c.N, K, c.extra, avg / iters, ms, flops / (ms * 1e-3) / 1e12);
+  }
   return 0;
 }
