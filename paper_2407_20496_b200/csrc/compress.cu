@@ -708,6 +708,33 @@ __global__ void __launch_bounds__(NT) k_nm_select_rows(const uint16_t* __restric
     }
     __syncthreads();
     const int64_t rbase = out_base + (int64_t)r * G * N;
+    if (M == 4 && N == 2) {
+      // 2:4: integer compares on |bf16| bits (monotone in |x|, same order as the fp64 saliency)
+      for (int g = threadIdx.x; g < G; g += NT) {
+        const int4 c4 = reinterpret_cast<const int4*>(s_idx)[g];
+        const uint16_t v0 = s_row[c4.x], v1 = s_row[c4.y], v2 = s_row[c4.z], v3 = s_row[c4.w];
+        const uint32_t a0 = v0 & 0x7FFFu, a1 = v1 & 0x7FFFu, a2 = v2 & 0x7FFFu, a3 = v3 & 0x7FFFu;
+        // rank_i = #{j : a_j > a_i or (a_j == a_i and j < i)}; keep rank < 2
+        const int r0 = (a1 > a0) + (a2 > a0) + (a3 > a0);
+        const int r1 = (a0 >= a1) + (a2 > a1) + (a3 > a1);
+        const int r2 = (a0 >= a2) + (a1 >= a2) + (a3 > a2);
+        const int r3 = (a0 >= a3) + (a1 >= a3) + (a2 >= a3);
+        int p0, p1;
+        uint16_t k0, k1;
+        if (r0 < 2) {
+          p0 = 0; k0 = v0;
+          if (r1 < 2) { p1 = 1; k1 = v1; } else if (r2 < 2) { p1 = 2; k1 = v2; } else { p1 = 3; k1 = v3; }
+        } else if (r1 < 2) {
+          p0 = 1; k0 = v1;
+          if (r2 < 2) { p1 = 2; k1 = v2; } else { p1 = 3; k1 = v3; }
+        } else {
+          p0 = 2; k0 = v2; p1 = 3; k1 = v3;
+        }
+        reinterpret_cast<uint16_t*>(nm_pos + rbase)[g] = (uint16_t)(p0 | (p1 << 8));
+        reinterpret_cast<uint32_t*>(kept + rbase)[g] = (uint32_t)k0 | ((uint32_t)k1 << 16);
+      }
+      continue;
+    }
     for (int g = threadIdx.x; g < G; g += NT) {
       const int32_t* cols = s_idx + g * M;
       uint16_t v[32];
@@ -739,20 +766,35 @@ __global__ void __launch_bounds__(NT) k_nm_select_rows(const uint16_t* __restric
 //   a_meta, per tile / 128-K block: V TMEM lanes x 4 words (word w = MMA step w of the block).
 //   Row m = m0 + 8*m1 + 16*m2 at K-half k1 lives in lane m0 + 8*k1 + 16*m2, bits 16*m1 + 4*c,
 //   nibble = p0 | p1 << 2 (cute TensorEAtom_MMA_F16 / tmem_e_frg, flashinfer-vendored CUTLASS).
-__global__ void k_pack_offsets(const int32_t* __restrict__ tile_ptr, int T,
-                               int32_t* __restrict__ kofs, int32_t* __restrict__ eofs) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int32_t ka = 0, ea = 0;
-  for (int t = 0; t < T; ++t) {
-    kofs[t] = ka;
-    eofs[t] = ea;
-    int k = tile_ptr[t + 1] - tile_ptr[t];
-    int kp = (int)round_up(k, 64);
-    ka += kp;
-    ea += (int)ceil_div(kp, 128);
+template <int NT>
+__global__ void __launch_bounds__(NT) k_pack_offsets(const int32_t* __restrict__ tile_ptr, int T,
+                                                     int32_t* __restrict__ kofs,
+                                                     int32_t* __restrict__ eofs) {
+  typedef cub::BlockScan<int, NT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int carry_k, carry_e;
+  if (threadIdx.x == 0) { carry_k = 0; carry_e = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += NT) {
+    const int t = base + threadIdx.x;
+    int kp = 0, eb = 0;
+    if (t < T) {
+      kp = (int)round_up(tile_ptr[t + 1] - tile_ptr[t], 64);
+      eb = (int)ceil_div(kp, 128);
+    }
+    int ek, ee, tk, te;
+    BS(tmp).ExclusiveSum(kp, ek, tk);
+    __syncthreads();
+    BS(tmp).ExclusiveSum(eb, ee, te);
+    if (t < T) {
+      kofs[t] = carry_k + ek;
+      eofs[t] = carry_e + ee;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { carry_k += tk; carry_e += te; }
+    __syncthreads();
   }
-  kofs[T] = ka;
-  eofs[T] = ea;
+  if (threadIdx.x == 0) { kofs[T] = carry_k; eofs[T] = carry_e; }
 }
 
 __device__ __forceinline__ int64_t aval_offset(int64_t kofs_t, int V, int r, int kc) {
@@ -1115,7 +1157,7 @@ extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
   int64_t kcap = 0, mcap = 0, acap = 0;
   hinm_pack_capacity(p->m, p->n, V, p->total_keep, &kcap, &mcap, &acap);
   if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
-  k_pack_offsets<<<1, 32, 0, stream>>>(p->tile_ptr, T, p->tile_kofs, p->tile_eofs);
+  k_pack_offsets<256><<<1, 256, 0, stream>>>(p->tile_ptr, T, p->tile_kofs, p->tile_eofs);
   HINM_LAUNCH_CHECK();
   HINM_CUDA_TRY(cudaMemsetAsync(p->a_vals, 0, (size_t)acap * 2, stream));
   const int64_t groups = p->total_keep / 4;

@@ -130,6 +130,17 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// parity to wait on for the n-th (0-based) use of a buffer guarded by an "empty" barrier
+__device__ __forceinline__ uint32_t phase_acc_empty_parity(uint32_t n) { return (n & 1) ^ 1; }
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -305,36 +316,40 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
 
   if (warp == AE_WARP) {
     // ============================================================ A / metadata producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      UnitParams nxt = unit_params(p, blockIdx.x);
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const UnitParams cur = nxt;
-        nxt = unit_params(p, u + gridDim.x);
-        const int k0 = cur.k0, kp = cur.kp, e0 = cur.e0;
-        for (int s = 0; s < kp / BK; ++s) {
-          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-          const uint32_t fb = bar_full + 8 * stage;
-          const uint32_t a_bytes = V * 64, e_bytes = (s & 1) ? 0 : V * 16;
+    // warp-uniform loop; one elected lane issues the bulk copies (see the MMA issuer note)
+    int stage = 0;
+    uint32_t phase = 0;
+    UnitParams nxt = unit_params(p, blockIdx.x);
+    const uint32_t a_bytes = V * 64;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const UnitParams cur = nxt;
+      nxt = unit_params(p, u + gridDim.x);
+      const int nst = cur.kp / BK;
+      const uint16_t* asrc = p.a_vals + (int64_t)cur.k0 * V / 2;
+      const uint32_t* esrc0 = p.a_meta + (int64_t)cur.e0 * V * 4;
+      for (int s = 0; s < nst; ++s) {
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        const uint32_t fb = bar_full + 8 * stage;
+        if (elect_one()) {
           if (DBG == 3) {  // experiment: no operand loads at all
             mbar_arrive(fb);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
-          bulk_g2s(sA + stage * V * 64, p.a_vals + (int64_t)(k0 + s * BK) * V / 2, a_bytes, fb);
-          if (e_bytes) {
-            const uint32_t* esrc = p.a_meta + ((int64_t)e0 + s / 2) * V * 4;
-            if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
-              for (int q = 0; q < V / 16; ++q)
-                bulk_g2s(sE + stage * E_STAGE + q * 512, esrc + q * 64, 256, fb);
-            } else {
-              bulk_g2s(sE + stage * E_STAGE, esrc, e_bytes, fb);
+          } else {
+            const uint32_t e_bytes = (s & 1) ? 0 : V * 16;
+            mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
+            bulk_g2s(sA + stage * a_bytes, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
+            if (e_bytes) {
+              const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
+              if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
+                for (int q = 0; q < V / 16; ++q)
+                  bulk_g2s(sE + stage * E_STAGE + q * 512, esrc + q * 64, 256, fb);
+              } else {
+                bulk_g2s(sE + stage * E_STAGE, esrc, e_bytes, fb);
+              }
             }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp >= GATHER_WARP0) {
@@ -430,42 +445,53 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     }
   } else if (warp == MMA_WARP) {
     // ============================================================ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(M64 ? 64 : 128, BN);
-      int stage = 0;
-      uint32_t phase = 0, eslot = 0, ucount = 0;
-      UnitParams nxt = unit_params(p, blockIdx.x);
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int kp = nxt.kp;
-        nxt = unit_params(p, u + gridDim.x);
-        if (kp == 0) continue;
-        const uint32_t acc = ucount % NACC, use = ucount / NACC;
-        ++ucount;
-        mbar_wait(bar_acc_empty + 8 * acc, (use & 1) ^ 1);
+    // The whole warp runs the loop (warp-uniform control flow keeps every descriptor in uniform
+    // registers); one elected lane issues the tcgen05 instructions.  A single-lane loop forced
+    // R2UR conversions of every operand per MMA and measured 2.6x slower MMA issue
+    // (scripts/mma_bench.cu vs mma_bench_v1.cu).
+    const uint32_t idesc = make_idesc(M64 ? 64 : 128, BN);
+    // descriptors at stage 0; the start-address field (16 B units, bits 0-13) is advanced by
+    // adding byte offsets >> 4
+    const uint64_t a_desc0 = smem_desc(sA, 128, 256, 0);
+    const uint64_t b_desc0 = smem_desc(sB, B_STAGE / 4, 1024, 2);
+    const uint64_t e_desc0 = smem_desc(sE, 0, 128, 0);
+    const uint32_t a_step = (uint32_t)(V * 64) >> 4, a_half = (uint32_t)(32 * V) >> 4;
+    int stage = 0;
+    uint32_t phase = 0, eslot = 0, acc_uses = 0;
+    UnitParams nxt = unit_params(p, blockIdx.x);
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int kp = nxt.kp;
+      nxt = unit_params(p, u + gridDim.x);
+      if (kp == 0) continue;
+      const uint32_t acc = 0;
+      mbar_wait(bar_acc_empty, phase_acc_empty_parity(acc_uses));
+      ++acc_uses;
+      tc_fence_after();
+      const int nst = kp / BK;
+      for (int s = 0; s < nst; ++s) {
+        mbar_wait(bar_full + 8 * stage, phase);
         tc_fence_after();
-        const uint32_t tmem_d = tmem + ((acc * 16u) << 16);
-        for (int s = 0; s < kp / BK; ++s) {
-          mbar_wait(bar_full + 8 * stage, phase);
-          tc_fence_after();
+        if (elect_one()) {
           if ((s & 1) == 0) {
-            eslot = (eslot + 1) % E_SLOTS;
-            // 128 lanes x 16 B: K-major no-swizzle core matrices, 8-row groups at 128 B
-            tmem_cp_128x128b(tmem + E_COL + eslot * 4, smem_desc(sE + stage * E_STAGE, 0, 128, 0));
+            eslot = (eslot + 1) & (E_SLOTS - 1);
+            tmem_cp_128x128b(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((stage * E_STAGE) >> 4));
           }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2 + j;
-            const uint64_t a_desc = smem_desc(sA + stage * V * 64 + j * 32 * V, 128, 256, 0);
-            const uint64_t b_desc = smem_desc(sB + stage * B_STAGE + j * 4096, B_STAGE / 4, 1024, 2);
-            if (DBG != 1) mma_sp(tmem_d, a_desc, b_desc, idesc | (ecol & 1u), ecol & ~1u, (s | j) ? 1u : 0u);
+          const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2;
+          const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
+          if (DBG != 1) {
+            mma_sp(tmem, ad, bd, idesc, ecol, s ? 1u : 0u);                       // id2 = 0
+            mma_sp(tmem, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);    // id2 = 1
           }
           tc_commit(bar_empty + 8 * stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(bar_acc_full + 8 * acc);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) tc_commit(bar_acc_full);
+      __syncwarp();
+      (void)acc;
     }
-    __syncwarp();
   } else {
     // ============================================================ epilogue (warps 0-3)
     const int q = warp;  // TMEM lane quadrant of this warp
