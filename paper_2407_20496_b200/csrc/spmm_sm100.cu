@@ -257,13 +257,11 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
 // M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
-// TG (cp.async mode): the first TG 8-row groups of every stage are gathered by an extra warp
-// with TMA gather4 (its own request path), the rest by the 8 cp.async warps.
-template <int MODE, int GW, int DBG = 0, bool M64 = false, int TG = 0>
-__global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1)
+template <int MODE, int GW, int DBG = 0, bool M64 = false>
+__global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
                 int64_t ldx, Params p) {
-  constexpr int NT = 32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0));
+  constexpr int NT = 32 * (GATHER_WARP0 + GW);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -301,7 +299,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
       mbar_init(bar_acc_empty + 8 * a, n_epi_warps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (MODE == GATHER_TMA || TG > 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+    if (MODE == GATHER_TMA) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == MMA_WARP) {
@@ -337,7 +335,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
             mbar_arrive(fb);
           } else {
             const uint32_t e_bytes = (s & 1) ? 0 : V * 16;
-            mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : TG * 8 * 512));
+            mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
             bulk_g2s(sA + stage * a_bytes, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
             if (e_bytes) {
               const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
@@ -354,67 +352,6 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (TG > 0 && warp == GATHER_WARP0 + GW) {
-    // ============================================================ TMA gather warp
-    // rows 0 .. 8*TG-1 of every stage: lane < 2*TG owns one quad of rows x 4 token sub-blocks
-    constexpr int PFT = 8;
-    const int dt = gridDim.x % T, dnb = gridDim.x / T;
-    int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pnst = 0;
-    auto next_unit = [&]() {
-      while (pu < p.units) {
-        pk0 = __ldg(p.tile_kofs + pt);
-        pnst = (__ldg(p.tile_kofs + pt + 1) - pk0) / BK;
-        if (pnst > 0) break;
-        pu += gridDim.x;
-        pt += dt;
-        pnb += dnb;
-        if (pt >= T) { pt -= T; ++pnb; }
-      }
-      ps = 0;
-    };
-    next_unit();
-    int4 r_quad[PFT];
-    int r_col[PFT];
-    bool r_ok[PFT];
-    auto prefetch = [&](int slot) {
-#pragma unroll
-      for (int j = 0; j < PFT; ++j) {
-        if (j != slot) continue;
-        r_ok[j] = pu < p.units;
-        if (!r_ok[j]) return;
-        r_col[j] = pnb * BN;
-        const int* gi = p.gidx + pk0 + ps * BK;
-        r_quad[j] = lane < 2 * TG ? __ldg(reinterpret_cast<const int4*>(gi) + lane) : make_int4(0, 0, 0, 0);
-        if (++ps == pnst) {
-          pu += gridDim.x;
-          pt += dt;
-          pnb += dnb;
-          if (pt >= T) { pt -= T; ++pnb; }
-          next_unit();
-        }
-      }
-    };
-#pragma unroll
-    for (int j = 0; j < PFT; ++j) prefetch(j);
-    int stage = 0;
-    uint32_t phase = 0;
-    bool done = false;
-    while (!done) {
-#pragma unroll
-      for (int j = 0; j < PFT; ++j) {
-        if (!r_ok[j]) { done = true; break; }
-        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-        if (lane < 2 * TG && DBG != 2 && DBG != 3) {
-#pragma unroll
-          for (int q = 0; q < BN / 64; ++q)
-            tma_gather4(sB + stage * B_STAGE + q * (B_STAGE / 4) + lane * 512, &xmap,
-                        r_col[j] + q * 64, r_quad[j], bar_full + 8 * stage);
-        }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        prefetch(j);
-      }
-    }
   } else if (warp >= GATHER_WARP0) {
     // ============================================================ gather producers
     // Flattened stream over (unit, stage) with the gather indices of stage i+PF loaded while
@@ -423,7 +360,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
     // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.
     const int gw = warp - GATHER_WARP0;
     constexpr int PF = 8;
-    constexpr int RPW = BK / GW - TG;  // K-rows per warp per stage (rows 8i + gw, i >= TG)
+    constexpr int RPW = BK / GW;  // K-rows per warp per stage
     static_assert(MODE == GATHER_TMA || GW == 8, "cp.async producer assumes 8 gather warps");
     const int dt = gridDim.x % T, dnb = gridDim.x / T;
     // prefetch cursor: unit (pt, pnb) with running index pu, stage ps of pnst
@@ -453,7 +390,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
         r_col[j] = pnb * BN;
         const int* gi = p.gidx + pk0 + ps * BK;
         if (MODE == GATHER_CPASYNC) {
-          r_row[j] = lane < RPW ? __ldg(gi + gw + (lane + TG) * GW) : 0;
+          r_row[j] = lane < RPW ? __ldg(gi + gw + lane * GW) : 0;
         } else {
           const int g = gw * 32 + lane;
           r_quad[j] = g < 64 ? __ldg(reinterpret_cast<const int4*>(gi) + (g >> 2)) : make_int4(0, 0, 0, 0);
@@ -486,7 +423,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW + (TG > 0 ? 1 : 0)), 1
           const int tok = col0 + lane * 8;
           const uint32_t src_bytes = tok < p.B ? 16u : 0u;
           const char* xs = xbase + (src_bytes ? (int64_t)tok * 2 : 0);
-          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane + TG * 1024;
+          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
           const int my_row = r_row[j];
 #pragma unroll
           for (int i = 0; i < RPW; ++i) {
@@ -710,9 +647,6 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "m128")) return 6;
     if (!strcmp(e, "dbg_noload")) return 7;
     if (!strcmp(e, "dbg_noload128")) return 8;
-    if (!strcmp(e, "mix1")) return 9;
-    if (!strcmp(e, "mix2")) return 10;
-    if (!strcmp(e, "mix3")) return 11;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
@@ -731,9 +665,6 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 6: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8); break;  // M=128 for any V
     case 7: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, true>, 8); break;
     case 8: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, false>, 8); break;
-    case 9: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true, 1>, 9); break;
-    case 10: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true, 2>, 9); break;
-    case 11: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true, 3>, 9); break;
     default:
       rc = pk->V <= 64 ? launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true>, 8)
                        : launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8);
