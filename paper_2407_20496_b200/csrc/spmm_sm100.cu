@@ -218,7 +218,7 @@ constexpr int MMA_WARP = 4;
 constexpr int AE_WARP = 5;
 constexpr int GATHER_WARP0 = 6;
 
-enum GatherMode : int { GATHER_CPASYNC = 0, GATHER_TMA = 1 };
+enum GatherMode : int { GATHER_CPASYNC = 0, GATHER_TMA = 1, GATHER_LDG = 2 };
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // cp.async mode: 1 expect_tx arrive + one noinc arrive per gather thread
-      mbar_init(bar_full + 8 * s, MODE == GATHER_CPASYNC ? 1 + 32 * GW : 1);
+      mbar_init(bar_full + 8 * s, MODE != GATHER_TMA ? 1 + 32 * GW : 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     const int gw = warp - GATHER_WARP0;
     constexpr int PF = 8;
     constexpr int RPW = BK / GW;  // K-rows per warp per stage
-    static_assert(MODE == GATHER_TMA || GW == 8, "cp.async producer assumes 8 gather warps");
+    static_assert(MODE == GATHER_TMA || GW == 8, "cp.async/LDG producers assume 8 gather warps");
     const int dt = gridDim.x % T, dnb = gridDim.x / T;
     // prefetch cursor: unit (pt, pnb) with running index pu, stage ps of pnst
     int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pnst = 0;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (!r_ok[j]) return;
         r_col[j] = pnb * BN;
         const int* gi = p.gidx + pk0 + ps * BK;
-        if (MODE == GATHER_CPASYNC) {
+        if (MODE != GATHER_TMA) {
           r_row[j] = lane < RPW ? __ldg(gi + gw + lane * GW) : 0;
         } else {
           const int g = gw * 32 + lane;
@@ -413,7 +413,47 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     int stage = 0;
     uint32_t phase = 0;
     bool done = false;
-    while (!done) {
+    if (MODE == GATHER_LDG) {
+      // register-staged gather: the rows of stage i+1 are loaded (LDG) before waiting for the
+      // stage-i slot, adding one stage of in-flight data held in registers
+      uint4 bufA[RPW], bufB[RPW];
+      auto ldg_rows = [&](uint4 (&buf)[RPW], int slot) {
+#pragma unroll
+        for (int jj = 0; jj < PF; ++jj) {
+          if (jj != slot) continue;
+          const int tok = r_col[jj] + lane * 8;
+          const bool in = r_ok[jj] && tok < p.B;
+#pragma unroll
+          for (int i = 0; i < RPW; ++i) {
+            const int row = __shfl_sync(0xffffffffu, r_row[jj], i);
+            buf[i] = in ? __ldg(reinterpret_cast<const uint4*>(xbase + row * ldx2 + (int64_t)tok * 2))
+                        : make_uint4(0, 0, 0, 0);
+          }
+        }
+      };
+      ldg_rows(bufA, 0);
+      while (!done) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+          if (!r_ok[j]) { done = true; break; }
+          uint4(&cur)[RPW] = (j & 1) ? bufB : bufA;
+          uint4(&nxt)[RPW] = (j & 1) ? bufA : bufB;
+          ldg_rows(nxt, (j + 1) % PF);
+          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
+#pragma unroll
+          for (int i = 0; i < RPW; ++i)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst0 + i * 1024),
+                         "r"(cur[i].x), "r"(cur[i].y), "r"(cur[i].z), "r"(cur[i].w)
+                         : "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(bar_full + 8 * stage);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          prefetch(j);
+        }
+      }
+    }
+    while (MODE != GATHER_LDG && !done) {
 #pragma unroll
       for (int j = 0; j < PF; ++j) {
         if (!r_ok[j]) { done = true; break; }
@@ -645,6 +685,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_nomma")) return 4;
     if (!strcmp(e, "dbg_nogather")) return 5;
     if (!strcmp(e, "m128")) return 6;
+    if (!strcmp(e, "ldg8")) return 9;
     if (!strcmp(e, "dbg_noload")) return 7;
     if (!strcmp(e, "dbg_noload128")) return 8;
     return 0;
@@ -665,6 +706,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     case 6: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8); break;  // M=128 for any V
     case 7: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, true>, 8); break;
     case 8: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, false>, 8); break;
+    case 9: rc = launch(k_hinm_spmm<GATHER_LDG, 8, 0, true>, 8); break;
     default:
       rc = pk->V <= 64 ? launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true>, 8)
                        : launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8);
