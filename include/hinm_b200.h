@@ -157,6 +157,29 @@ int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t* sigma_o,
 int hinm_spmm_bf16(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
                    uint16_t* Y, int64_t ldy, int out_order, void* stream);
 
+/*
+ * End-to-end execution from HOST buffers (the user-facing call of the reference, spmm.py:75-99,
+ * for a chain of layers as in spmm.py:206-244 / cli.py:234-249): buffer 0 is the chain input X
+ * (buf_rows[0] x B, host, leading dim ldx), every step computes buf[dst] = W(pack) @ buf[src],
+ * and buffer out_buf is copied back to Y_host (buf_rows[out_buf] x B, leading dim ldy).  Tokens
+ * are processed in chunks of chunk_tokens; H2D, SpMMs and D2H of consecutive chunks overlap on
+ * two internal copy streams and `stream`.  Host buffers must be page-locked for the copies to
+ * overlap.  Work completes on `stream` (async w.r.t. the host).  B % 8 == 0, chunk % 8 == 0.
+ */
+typedef struct {
+  const hinm_pack_t* pack;
+  int32_t src, dst;
+  int32_t out_order;
+} hinm_chain_step_t;
+
+/* Device workspace of hinm_chain_run_host: 3 chunk slots x sum(buf_rows) x chunk bf16. */
+int hinm_chain_workspace(const int64_t* buf_rows, int nbuf, int chunk_tokens, size_t* bytes);
+
+int hinm_chain_run_host(const hinm_chain_step_t* steps, int nsteps, const int64_t* buf_rows,
+                        int nbuf, int out_buf, const uint16_t* X_host, int64_t ldx, int B,
+                        uint16_t* Y_host, int64_t ldy, int chunk_tokens, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* Same product from the reference view on CUDA cores, fp32 out (test cross-check). Async. */
 int hinm_spmm_simt_f32(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
                        float* Y, int64_t ldy, int out_order, void* stream);

@@ -17,7 +17,7 @@ from .pruning import (HiNMEncoding, TileEncoding, apply_masks, decode, encode, e
                       restore_row_order, survivors_per_tile, validate_masks, vector_prune)
 from .spmm import (TileBuffer, dense_matmul, gather_tile_buffer, hinm_spmm,
                    hinm_spmm_original_order, relative_error)
-from .device import DevicePack, build_operand_image, compress, spmm, spmm_simt
+from .device import DevicePack, HostChain, build_operand_image, compress, spmm, spmm_simt
 
 __version__ = "0.1.0"
 
@@ -31,5 +31,5 @@ __all__ = [
     "masked_dense_from_encoding", "nm_prune", "restore_row_order", "survivors_per_tile",
     "validate_masks", "vector_prune", "TileBuffer", "dense_matmul", "gather_tile_buffer",
     "hinm_spmm", "hinm_spmm_original_order", "relative_error", "DevicePack",
-    "build_operand_image", "compress", "spmm", "spmm_simt",
+    "build_operand_image", "compress", "spmm", "spmm_simt", "HostChain",
 ]

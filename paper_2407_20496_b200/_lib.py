@@ -50,6 +50,13 @@ class PackStruct(ctypes.Structure):
     ]
 
 
+class ChainStep(ctypes.Structure):
+    """Mirror of hinm_chain_step_t."""
+
+    _fields_ = [("pack", ctypes.POINTER(PackStruct)), ("src", ctypes.c_int32),
+                ("dst", ctypes.c_int32), ("out_order", ctypes.c_int32)]
+
+
 _SIGNATURES = {
     "hinm_version": ([], ctypes.c_char_p),
     "hinm_status_string": ([c_int], ctypes.c_char_p),
@@ -68,6 +75,9 @@ _SIGNATURES = {
                        c_int),
     "hinm_spmm_simt_f32": ([ctypes.POINTER(PackStruct), c_vp, c_i64, c_int, c_vp, c_i64, c_int,
                             c_vp], c_int),
+    "hinm_chain_workspace": ([ctypes.POINTER(c_i64), c_int, c_int, ctypes.POINTER(c_size)], c_int),
+    "hinm_chain_run_host": ([ctypes.POINTER(ChainStep), c_int, ctypes.POINTER(c_i64), c_int, c_int,
+                             c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_size, c_vp], c_int),
     "hinm_last_launch_count": ([], c_int),
 }
 EXPORTED = tuple(_SIGNATURES)

@@ -267,3 +267,75 @@ def spmm_simt(pack: DevicePack, X, order: str = "sigma"):
                                               out.data_ptr(), out.stride(0), ordv,
                                               _stream_handle(X.device)), "spmm_simt")
     return out
+
+
+class HostChain:
+    """End-to-end SpMM chain from HOST buffers (hinm_chain_run_host).
+
+    ``steps`` = [(pack, src, dst, order)], buffer 0 = the chain input (host X), ``out_buf`` = the
+    buffer copied back to the host.  Tokens run in chunks of ``chunk`` with H2D / SpMM / D2H of
+    consecutive chunks overlapped on three streams; the device workspace (3 chunk slots) is
+    allocated once here.  Host tensors should be pinned (``pin_memory()``) for the overlap.
+    """
+
+    def __init__(self, steps, out_buf: int, chunk: int = 2048, device=None):
+        torch = _torch()
+        if not steps:
+            raise ValueError("empty chain")
+        self.device = torch.device(device) if device is not None else steps[0][0].device
+        rows = {}
+        for pack, src, dst, _ in steps:
+            for b, r in ((src, pack.n), (dst, pack.m)):
+                if rows.setdefault(b, r) != r:
+                    raise ShapeMismatch(f"buffer {b} used with {rows[b]} and {r} rows")
+        nbuf = max(rows) + 1
+        if sorted(rows) != list(range(nbuf)) or not 0 < out_buf < nbuf:
+            raise ValueError("chain buffers must be numbered 0..nbuf-1 with 0 the input")
+        self.nbuf, self.out_buf, self.chunk = nbuf, out_buf, chunk
+        self.buf_rows = (ctypes.c_int64 * nbuf)(*[rows[b] for b in range(nbuf)])
+        self._structs = [p.struct() for p, _, _, _ in steps]
+        self._packs = [p for p, _, _, _ in steps]
+        self.steps = (_lib.ChainStep * len(steps))()
+        for i, (_, src, dst, order) in enumerate(steps):
+            self.steps[i].pack = ctypes.pointer(self._structs[i])
+            self.steps[i].src, self.steps[i].dst = src, dst
+            self.steps[i].out_order = (_lib.HINM_ORDER_ORIGINAL if order == "original"
+                                       else _lib.HINM_ORDER_SIGMA)
+        lib = _lib.load()
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.hinm_chain_workspace(self.buf_rows, nbuf, chunk, ctypes.byref(nbytes)),
+                   "chain_workspace")
+        self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
+
+    @property
+    def in_rows(self) -> int:
+        return int(self.buf_rows[0])
+
+    @property
+    def out_rows(self) -> int:
+        return int(self.buf_rows[self.out_buf])
+
+    def run(self, X_host, out=None):
+        """Y_host = chain(X_host); X_host is an (in_rows x B) bf16 CPU tensor.  Completes on the
+        current CUDA stream (synchronize before reading ``out``)."""
+        torch = _torch()
+        if X_host.is_cuda or X_host.dtype != torch.bfloat16 or X_host.dim() != 2:
+            raise ValueError("X_host must be a 2-D bfloat16 CPU tensor")
+        if X_host.shape[0] != self.in_rows:
+            raise ShapeMismatch(f"input has {X_host.shape[0]} rows, chain expects {self.in_rows}")
+        B = X_host.shape[1]
+        if out is None:
+            out = torch.empty(self.out_rows, B, dtype=torch.bfloat16, pin_memory=True)
+        if X_host.stride(1) != 1:
+            raise ValueError("X_host rows must be contiguous")
+        if tuple(out.shape) != (self.out_rows, B) or out.is_cuda or out.stride(1) != 1:
+            raise ShapeMismatch("out must be a host (out_rows x B) bf16 tensor")
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            status = lib.hinm_chain_run_host(self.steps, len(self._structs), self.buf_rows,
+                                             self.nbuf, self.out_buf, X_host.data_ptr(),
+                                             X_host.stride(0), B, out.data_ptr(), out.stride(0),
+                                             self.chunk, self.workspace.data_ptr(),
+                                             self.workspace.numel(), _stream_handle(self.device))
+        _lib.check(status, "chain_run_host")
+        return out
