@@ -30,9 +30,14 @@ namespace hinm {
 namespace sm100 {
 
 constexpr int BN = 256;                        // tokens per unit (UMMA N)
-constexpr int BK = 64;                         // logical K per pipeline stage
-constexpr int STAGES = 5;
-constexpr int B_STAGE = BK * BN * 2;           // 32 KB of gathered X per stage
+constexpr int BK = 64;                         // logical K per A / metadata stage (2 MMAs)
+constexpr int MAX_ASTAGES = 12;                // compressed-A / metadata ring (own barriers)
+// Gathered-X ring: KS K-rows (x 256 tokens) per stage.  The cp.async gather pays a fixed
+// per-stage cost in every producer warp (barrier wait + arrive), so 128-row stages
+// (16 warps x 8 rows) stream markedly faster than 64-row ones (scripts/l2_ring.cu on B200:
+// 20.4 vs 16.6 TB/s).
+__host__ __device__ constexpr int b_stages(int KS) { return KS == 128 ? 3 : 5; }
+__host__ __device__ constexpr int b_stage_bytes(int KS) { return KS * BN * 2; }
 constexpr int E_STAGE = 128 * 16;              // 128 lanes x 16 B metadata image per stage slot
 constexpr int TMEM_COLS = 512;
 constexpr int E_COL = 256;                     // metadata ring after the 256-column accumulator
@@ -56,15 +61,23 @@ struct Params {
 };
 
 struct SmemLayout {
-  uint32_t a, e, bar, tmem, total;
+  uint32_t a, e, bar, tmem, total, ast;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int V) {
+// The A / metadata ring is decoupled from the gathered-X ring and deeper: its bulk copies see a
+// much longer latency than the cp.async gather under load, and with a shared barrier they held
+// every X stage hostage (scripts/l2_ring.cu).  Depth = whatever fits next to the X ring.
+__host__ __device__ inline SmemLayout smem_layout(int V, int KS) {
   SmemLayout L;
-  L.a = STAGES * B_STAGE;
-  L.e = L.a + STAGES * V * 64 + 4096;          // 4 KB slack: M=128 descriptor over-read
-  L.bar = L.e + STAGES * E_STAGE;
-  L.tmem = L.bar + (2 * STAGES + 4) * 8;
+  const uint32_t budget = 227 * 1024 - 1024 - 4096 - 512;
+  const uint32_t per = V * 64 + E_STAGE;
+  const uint32_t xring = b_stages(KS) * b_stage_bytes(KS);
+  const uint32_t fit = (budget - xring) / per;
+  L.ast = fit < (uint32_t)MAX_ASTAGES ? fit : MAX_ASTAGES;
+  L.a = xring;
+  L.e = L.a + L.ast * V * 64 + 4096;           // 4 KB slack: M=128 descriptor over-read
+  L.bar = L.e + L.ast * E_STAGE;
+  L.tmem = L.bar + (2 * 5 + 2 * MAX_ASTAGES + 2) * 8;
   L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
   return L;
 }
@@ -118,15 +131,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int4 rows,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(map), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w), "r"(bar)
       : "memory");
 }
 
@@ -191,16 +195,23 @@ __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc)
   asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
+// 16 lanes x (32 + 32) columns: thread l < 16 gets lane l, columns c..c+31; thread l >= 16 gets
+// lane l-16, columns c+128..c+159.
+__device__ __forceinline__ void tmem_ld_16x32bx2_x32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {"
+      "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 128;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 32 lanes x 32 columns: thread l gets lane l, columns c..c+31.
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {"
+      "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -212,13 +223,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32
 
 // ------------------------------------------------------------------------------ the kernel
 // Warp layout: warps 0-3 epilogue (TMEM lane quadrant = warp), warp 4 MMA issuer + TMEM owner,
-// warp 5 A/metadata producer (bulk copies), warps 6.. gather producers.
-constexpr int EPI_WARPS = 4;
+// warp 5 A/metadata producer (bulk copies), warps 6.. gather producers.  The gather rate scales
+// with the number of warps issuing cp.async, not with the bytes in flight (scripts/l2_cap.cu on
+// B200: 8 warps/SM 15.6 TB/s, 12 -> 19.2, 16 -> 21.0 TB/s at any depth), so the default runs
+// 16 gather warps.
 constexpr int MMA_WARP = 4;
 constexpr int AE_WARP = 5;
 constexpr int GATHER_WARP0 = 6;
-
-enum GatherMode : int { GATHER_CPASYNC = 0, GATHER_TMA = 1, GATHER_LDG = 2 };
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -257,49 +268,51 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
 // M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
-template <int MODE, int GW, int DBG = 0, bool M64 = false>
+template <int KS, int GW, int DBG = 0, bool M64 = false>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
-    k_hinm_spmm(const __grid_constant__ CUtensorMap xmap, const uint16_t* __restrict__ X,
-                int64_t ldx, Params p) {
+    k_hinm_spmm(const uint16_t* __restrict__ X, int64_t ldx, Params p) {
   constexpr int NT = 32 * (GATHER_WARP0 + GW);
+  constexpr int STAGES = b_stages(KS), B_STAGE = b_stage_bytes(KS);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const SmemLayout L = smem_layout(p.V);
+  const SmemLayout L = smem_layout(p.V, KS);
   const int V = p.V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
   const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
-  constexpr int NACC = 1;  // accumulator buffers
-  const uint32_t bar_acc_full = bar_empty + STAGES * 8;   // [NACC]
-  const uint32_t bar_acc_empty = bar_acc_full + 16;       // [NACC]
+  const uint32_t bar_afull = bar_empty + STAGES * 8, bar_aempty = bar_afull + MAX_ASTAGES * 8;
+  const uint32_t bar_acc_full = bar_aempty + MAX_ASTAGES * 8;
+  const uint32_t bar_acc_empty = bar_acc_full + 8;
+  const int AST = (int)L.ast;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
-  // warps (= TMEM lane quadrants) that hold real rows
-  const int n_epi_warps = M64 ? V / 16 : (V >= 128 ? 4 : V / 32);
+  // TMEM lane quadrants (= epilogue warps) that hold real rows
+  const int n_quads = M64 ? V / 16 : (V >= 128 ? 4 : V / 32);
+  const int n_epi_warps = n_quads;
 
   // constant metadata for lanes the producer never writes (rows >= V, M=64 gap lanes)
   if (M64) {
-    for (int i = threadIdx.x; i < STAGES * E_STAGE / 4; i += NT)
+    for (int i = threadIdx.x; i < AST * E_STAGE / 4; i += NT)
       reinterpret_cast<uint32_t*>(gbase + L.e)[i] = META_PAD;
   } else {
-    for (int i = threadIdx.x; i < STAGES * (128 - V) * 4; i += NT) {
+    for (int i = threadIdx.x; i < AST * (128 - V) * 4; i += NT) {
       const int s = i / ((128 - V) * 4), w = i % ((128 - V) * 4);
       reinterpret_cast<uint32_t*>(gbase + L.e + s * E_STAGE + V * 16)[w] = META_PAD;
     }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      // cp.async mode: 1 expect_tx arrive + one noinc arrive per gather thread
-      mbar_init(bar_full + 8 * s, MODE != GATHER_TMA ? 1 + 32 * GW : 1);
+      mbar_init(bar_full + 8 * s, 32 * GW);       // one cp.async noinc arrive per gather thread
       mbar_init(bar_empty + 8 * s, 1);
     }
-    for (int a = 0; a < NACC; ++a) {
-      mbar_init(bar_acc_full + 8 * a, 1);
-      mbar_init(bar_acc_empty + 8 * a, n_epi_warps);
+    for (int s = 0; s < AST; ++s) {
+      mbar_init(bar_afull + 8 * s, 1);
+      mbar_init(bar_aempty + 8 * s, 1);
     }
+    mbar_init(bar_acc_full, 1);
+    mbar_init(bar_acc_empty, n_epi_warps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (MODE == GATHER_TMA) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == MMA_WARP) {
@@ -317,8 +330,8 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   if (warp == AE_WARP) {
     // ============================================================ A / metadata producer
     // warp-uniform loop; one elected lane issues the bulk copies (see the MMA issuer note)
-    int stage = 0;
-    uint32_t phase = 0;
+    int aslot = 0;
+    uint32_t aphase = 0;
     UnitParams nxt = unit_params(p, blockIdx.x);
     const uint32_t a_bytes = V * 64;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -328,48 +341,45 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       const uint16_t* asrc = p.a_vals + (int64_t)cur.k0 * V / 2;
       const uint32_t* esrc0 = p.a_meta + (int64_t)cur.e0 * V * 4;
       for (int s = 0; s < nst; ++s) {
-        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-        const uint32_t fb = bar_full + 8 * stage;
+        mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
+        const uint32_t fb = bar_afull + 8 * aslot;
         if (elect_one()) {
-          if (DBG == 3) {  // experiment: no operand loads at all
-            mbar_arrive(fb);
-          } else {
-            const uint32_t e_bytes = (s & 1) ? 0 : V * 16;
-            mbar_expect_tx(fb, a_bytes + e_bytes + (MODE == GATHER_TMA ? B_STAGE : 0));
-            bulk_g2s(sA + stage * a_bytes, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
-            if (e_bytes) {
-              const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
-              if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
-                for (int q = 0; q < V / 16; ++q)
-                  bulk_g2s(sE + stage * E_STAGE + q * 512, esrc + q * 64, 256, fb);
-              } else {
-                bulk_g2s(sE + stage * E_STAGE, esrc, e_bytes, fb);
-              }
+          const uint32_t e_bytes = (s & 1) ? 0 : V * 16;
+          mbar_expect_tx(fb, a_bytes + e_bytes);
+          bulk_g2s(sA + aslot * a_bytes, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
+          if (e_bytes) {
+            const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
+            if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
+              for (int q = 0; q < V / 16; ++q)
+                bulk_g2s(sE + aslot * E_STAGE + q * 512, esrc + q * 64, 256, fb);
+            } else {
+              bulk_g2s(sE + aslot * E_STAGE, esrc, e_bytes, fb);
             }
           }
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
     }
   } else if (warp >= GATHER_WARP0) {
     // ============================================================ gather producers
-    // Flattened stream over (unit, stage) with the gather indices of stage i+PF loaded while
+    // Flattened stream over (unit, X stage) with the gather indices of stage i+PF loaded while
     // stage i is issued (the dependent index load never sits on the critical path).  The
     // issue loop is kept to ~4 instructions per 512-byte row: warp gw owns the K-rows
-    // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.
+    // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.  The last stage of a unit
+    // may be partial (kp is a multiple of 64, KS may be 128).
     const int gw = warp - GATHER_WARP0;
     constexpr int PF = 8;
-    constexpr int RPW = BK / GW;  // K-rows per warp per stage
-    static_assert(MODE == GATHER_TMA || GW == 8, "cp.async/LDG producers assume 8 gather warps");
+    constexpr int RPW = KS / GW;  // K-rows per warp per stage
+    static_assert(KS % GW == 0 && GW >= 8 && RPW <= 32, "gather producers: GW | KS, GW >= 8");
     const int dt = gridDim.x % T, dnb = gridDim.x / T;
-    // prefetch cursor: unit (pt, pnb) with running index pu, stage ps of pnst
-    int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pnst = 0;
+    // prefetch cursor: unit (pt, pnb) with running index pu, stage ps, kp of the unit
+    int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pkp = 0;
     auto next_unit = [&]() {  // advance to the next unit with work
       while (pu < p.units) {
         pk0 = __ldg(p.tile_kofs + pt);
-        pnst = (__ldg(p.tile_kofs + pt + 1) - pk0) / BK;
-        if (pnst > 0) break;
+        pkp = __ldg(p.tile_kofs + pt + 1) - pk0;
+        if (pkp > 0) break;
         pu += gridDim.x;
         pt += dt;
         pnb += dnb;
@@ -378,8 +388,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       ps = 0;
     };
     next_unit();
-    int r_row[PF], r_col[PF];
-    int4 r_quad[PF];
+    int r_row[PF], r_col[PF], r_n[PF];
     bool r_ok[PF];
     auto prefetch = [&](int slot) {
 #pragma unroll
@@ -388,14 +397,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         r_ok[j] = pu < p.units;
         if (!r_ok[j]) return;
         r_col[j] = pnb * BN;
-        const int* gi = p.gidx + pk0 + ps * BK;
-        if (MODE != GATHER_TMA) {
-          r_row[j] = lane < RPW ? __ldg(gi + gw + lane * GW) : 0;
-        } else {
-          const int g = gw * 32 + lane;
-          r_quad[j] = g < 64 ? __ldg(reinterpret_cast<const int4*>(gi) + (g >> 2)) : make_int4(0, 0, 0, 0);
-        }
-        if (++ps == pnst) {
+        const int n = min(KS, pkp - ps * KS);
+        r_n[j] = n;
+        const int* gi = p.gidx + pk0 + ps * KS;
+        r_row[j] = lane < RPW && gw + lane * GW < n ? __ldg(gi + gw + lane * GW) : 0;
+        if (++ps * KS >= pkp) {
           pu += gridDim.x;
           pt += dt;
           pnb += dnb;
@@ -406,79 +412,29 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     };
 #pragma unroll
     for (int j = 0; j < PF; ++j) prefetch(j);
-    // per-warp constant part of the SWIZZLE_128B destination (row r = gw + 8 i: r & 7 = gw)
-    const uint32_t dst_lane = (lane >> 3) * (B_STAGE / 4) + gw * 128 + (((lane & 7) ^ gw) << 4);
+    // per-warp constant part of the SWIZZLE_128B destination (row r = gw + GW i: r & 7 = gw & 7)
+    const uint32_t dst_lane = (lane >> 3) * (B_STAGE / 4) + gw * 128 + (((lane & 7) ^ (gw & 7)) << 4);
     const char* xbase = reinterpret_cast<const char*>(X);
     const int64_t ldx2 = ldx * 2;
     int stage = 0;
     uint32_t phase = 0;
     bool done = false;
-    if (MODE == GATHER_LDG) {
-      // register-staged gather: the rows of stage i+1 are loaded (LDG) before waiting for the
-      // stage-i slot, adding one stage of in-flight data held in registers
-      uint4 bufA[RPW], bufB[RPW];
-      auto ldg_rows = [&](uint4 (&buf)[RPW], int slot) {
-#pragma unroll
-        for (int jj = 0; jj < PF; ++jj) {
-          if (jj != slot) continue;
-          const int tok = r_col[jj] + lane * 8;
-          const bool in = r_ok[jj] && tok < p.B;
-#pragma unroll
-          for (int i = 0; i < RPW; ++i) {
-            const int row = __shfl_sync(0xffffffffu, r_row[jj], i);
-            buf[i] = in ? __ldg(reinterpret_cast<const uint4*>(xbase + row * ldx2 + (int64_t)tok * 2))
-                        : make_uint4(0, 0, 0, 0);
-          }
-        }
-      };
-      ldg_rows(bufA, 0);
-      while (!done) {
-#pragma unroll
-        for (int j = 0; j < PF; ++j) {
-          if (!r_ok[j]) { done = true; break; }
-          uint4(&cur)[RPW] = (j & 1) ? bufB : bufA;
-          uint4(&nxt)[RPW] = (j & 1) ? bufA : bufB;
-          ldg_rows(nxt, (j + 1) % PF);
-          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
-#pragma unroll
-          for (int i = 0; i < RPW; ++i)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst0 + i * 1024),
-                         "r"(cur[i].x), "r"(cur[i].y), "r"(cur[i].z), "r"(cur[i].w)
-                         : "memory");
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(bar_full + 8 * stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          prefetch(j);
-        }
-      }
-    }
-    while (MODE != GATHER_LDG && !done) {
+    while (!done) {
 #pragma unroll
       for (int j = 0; j < PF; ++j) {
         if (!r_ok[j]) { done = true; break; }
-        const int col0 = r_col[j];
+        const int tok = r_col[j] + lane * 8;
+        const uint32_t src_bytes = tok < p.B ? 16u : 0u;
+        const char* xs = xbase + (src_bytes ? (int64_t)tok * 2 : 0);
+        const int my_row = r_row[j], n = r_n[j];
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-        if (MODE == GATHER_CPASYNC) {
-          const int tok = col0 + lane * 8;
-          const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-          const char* xs = xbase + (src_bytes ? (int64_t)tok * 2 : 0);
-          const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
-          const int my_row = r_row[j];
+        const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
 #pragma unroll
-          for (int i = 0; i < RPW; ++i) {
-            const int row = __shfl_sync(0xffffffffu, my_row, i);
-            if (DBG != 2 && DBG != 3) cp_async_16(dst0 + i * 1024, xs + row * ldx2, src_bytes);
-          }
-          cp_async_arrive_noinc(bar_full + 8 * stage);
-        } else {
-          const int g = gw * 32 + lane;
-          if (g < 64) {
-            const int quad = g >> 2, q = g & 3;
-            tma_gather4(sB + stage * B_STAGE + q * (B_STAGE / 4) + quad * 512, &xmap,
-                        col0 + q * 64, r_quad[j], bar_full + 8 * stage);
-          }
+        for (int i = 0; i < RPW; ++i) {
+          const int row = __shfl_sync(0xffffffffu, my_row, i);
+          if (DBG != 2 && gw + i * GW < n) cp_async_16(dst0 + i * GW * 128, xs + row * ldx2, src_bytes);
         }
+        cp_async_arrive_noinc(bar_full + 8 * stage);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         prefetch(j);
       }
@@ -496,52 +452,79 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     const uint64_t b_desc0 = smem_desc(sB, B_STAGE / 4, 1024, 2);
     const uint64_t e_desc0 = smem_desc(sE, 0, 128, 0);
     const uint32_t a_step = (uint32_t)(V * 64) >> 4, a_half = (uint32_t)(32 * V) >> 4;
-    int stage = 0;
-    uint32_t phase = 0, eslot = 0, acc_uses = 0;
+    int stage = 0, aslot = 0;
+    uint32_t phase = 0, aphase = 0, eslot = 0, acc_uses = 0;
     UnitParams nxt = unit_params(p, blockIdx.x);
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int kp = nxt.kp;
       nxt = unit_params(p, u + gridDim.x);
       if (kp == 0) continue;
-      const uint32_t acc = 0;
       mbar_wait(bar_acc_empty, phase_acc_empty_parity(acc_uses));
       ++acc_uses;
       tc_fence_after();
       const int nst = kp / BK;
+      constexpr int SUB = KS / BK;  // A stages per X stage
       for (int s = 0; s < nst; ++s) {
-        mbar_wait(bar_full + 8 * stage, phase);
+        const int sub = s % SUB;
+        mbar_wait(bar_afull + 8 * aslot, aphase);
+        if (sub == 0) mbar_wait(bar_full + 8 * stage, phase);
         tc_fence_after();
         if (elect_one()) {
           if ((s & 1) == 0) {
             eslot = (eslot + 1) & (E_SLOTS - 1);
-            tmem_cp_128x128b(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((stage * E_STAGE) >> 4));
+            tmem_cp_128x128b(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((aslot * E_STAGE) >> 4));
           }
           const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2;
-          const uint64_t ad = a_desc0 + (uint64_t)(stage * a_step);
-          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
+          const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE + sub * BK * 128) >> 4);
           if (DBG != 1) {
             mma_sp(tmem, ad, bd, idesc, ecol, s ? 1u : 0u);                       // id2 = 0
             mma_sp(tmem, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);    // id2 = 1
           }
-          tc_commit(bar_empty + 8 * stage);
+          if (sub == SUB - 1 || s == nst - 1) tc_commit(bar_empty + 8 * stage);
+          tc_commit(bar_aempty + 8 * aslot);
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (sub == SUB - 1 || s == nst - 1) {
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
       if (elect_one()) tc_commit(bar_acc_full);
       __syncwarp();
-      (void)acc;
     }
   } else {
     // ============================================================ epilogue (warps 0-3)
-    const int q = warp;  // TMEM lane quadrant of this warp
-    if (q < n_epi_warps) {
+    // The accumulator is drained with 32-column tcgen05.ld's and released to the MMA issuer right
+    // after the LAST load, before that chunk's bf16 conversion and stores.
+    //   M=64 : row 16q + (lane & 15); chunk c = columns 32c + 128(lane >= 16) + [0, 32), c < 4
+    //          (16x32bx2: lanes 0-15 of the quadrant hold the 16 accumulator rows, so all 32
+    //          threads of the warp carry data)
+    //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c < 8   (32x32b)
+    const int q = warp;
+    if (q < n_quads) {
       uint32_t ucount = 0;
-      // row of this thread: M=128 -> lane; M=64 -> lanes 0-15 hold rows 16q + 0..15
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
-      auto out_row = [&](const UnitParams& q) -> int64_t {
-        const int64_t prow = (int64_t)q.t * V + r;
+      const int c_own = M64 && lane >= 16 ? 128 : 0;
+      constexpr int NCH = M64 ? 4 : 8;
+      const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16);
+      auto out_row = [&](const UnitParams& u) -> int64_t {
+        const int64_t prow = (int64_t)u.t * V + r;
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
+      };
+      // 32 accumulator columns (fp32 bits) -> bf16 -> 4 x 16-byte stores of one row segment
+      auto store32 = [&](uint16_t* yrow, int col, const uint32_t (&v)[32]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (col + j * 8 < p.B) {
+            uint4 o;
+            o.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+            o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+            o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+            o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+            *reinterpret_cast<uint4*>(yrow + col + j * 8) = o;
+          }
+        }
       };
       UnitParams nxt = unit_params(p, blockIdx.x);
       int64_t nxt_row = blockIdx.x < p.units ? out_row(nxt) : 0;
@@ -550,41 +533,31 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         const int64_t orow = nxt_row;
         nxt = unit_params(p, u + gridDim.x);
         if (u + (int)gridDim.x < p.units) nxt_row = out_row(nxt);
-        const int nb = cur.nb, kp = cur.kp;
         uint16_t* yrow = p.Y + orow * p.ldy;
-        const int col_base = nb * BN;
-        if (kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
-          if (M64 && lane >= 16) continue;
-          for (int c = 0; c < BN; c += 8)
-            if (col_base + c < p.B)
-              *reinterpret_cast<uint4*>(yrow + col_base + c) = make_uint4(0, 0, 0, 0);
+        const int col_base = cur.nb * BN + c_own;
+        if (cur.kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
+          for (int c = 0; c < NCH * 4; ++c)
+            if (col_base + c * 8 < p.B)
+              *reinterpret_cast<uint4*>(yrow + col_base + c * 8) = make_uint4(0, 0, 0, 0);
           continue;
         }
-        const uint32_t acc = ucount % NACC, use = ucount / NACC;
+        mbar_wait(bar_acc_full, ucount & 1);
         ++ucount;
-        const bool mine = !M64 || lane < 16;
-        mbar_wait(bar_acc_full + 8 * acc, use & 1);
         tc_fence_after();
+        uint32_t v[32];
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c * 32, v);
-          const int col = col_base + c * 32;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            if (mine && col + h * 8 < p.B) {
-              uint4 o;
-              o.x = pack_bf16x2(v[h * 8 + 0], v[h * 8 + 1]);
-              o.y = pack_bf16x2(v[h * 8 + 2], v[h * 8 + 3]);
-              o.z = pack_bf16x2(v[h * 8 + 4], v[h * 8 + 5]);
-              o.w = pack_bf16x2(v[h * 8 + 6], v[h * 8 + 7]);
-              *reinterpret_cast<uint4*>(yrow + col + h * 8) = o;
-            }
+        for (int c = 0; c < NCH; ++c) {
+          if (M64)
+            tmem_ld_16x32bx2_x32(t_row + c * 32, v);
+          else
+            tmem_ld_32x32b_x32(t_row + c * 32, v);
+          if (c == NCH - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_acc_empty);
           }
+          store32(yrow, col_base + c * 32, v);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
       }
     }
   }
@@ -601,24 +574,6 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
 
 // ------------------------------------------------------------------------------ host side
 namespace {
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)ptr;
-  }
-  return fn;
-}
 
 thread_local int g_last_launches = 0;
 
@@ -644,20 +599,6 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   if (B < 0 || (B % 8) || (ldx % 8) || (ldy % 8) || ldx < B || ldy < B) return HINM_ERR_VALUE;
   if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15)) return HINM_ERR_VALUE;
   if (B == 0 || pk->m == 0) return HINM_OK;
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return HINM_ERR_CUDA;
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)pk->n};
-  cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-  cuuint32_t box[2] = {64, 1};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)X, dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) {
-    fprintf(stderr, "[hinm] cuTensorMapEncodeTiled failed (%d)\n", (int)cr);
-    return HINM_ERR_CUDA;
-  }
   Params prm;
   prm.tile_kofs = pk->tile_kofs;
   prm.tile_eofs = pk->tile_eofs;
@@ -673,44 +614,43 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int nbk = (B + BN - 1) / BN;
   prm.units = nbk * pk->T;
   prm.out_order = out_order;
-  const SmemLayout L = smem_layout(pk->V);
   const int grid = std::min(prm.units, sm_count());
-  // variant: cp.async gather with 4 (default) or 8 warps, or TMA gather4 with 2 / 4 warps
+  // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 contend
+  // with the MMA for shared-memory bandwidth); V <= 64 -> 128-row X stages; V = 128 -> 64-row
+  // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
+  // Experiments: HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128 (M=128 instruction for
+  // V <= 64) | dbg_nomma | dbg_nogather (timing only: the results are garbage).
+  static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
+  static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
   static const int variant = [] {
     const char* e = getenv("HINM_GATHER");
     if (!e) return 0;
-    if (!strcmp(e, "cp8")) return 1;
-    if (!strcmp(e, "tma") || !strcmp(e, "tma2")) return 2;
-    if (!strcmp(e, "tma4")) return 3;
-    if (!strcmp(e, "dbg_nomma")) return 4;
-    if (!strcmp(e, "dbg_nogather")) return 5;
-    if (!strcmp(e, "m128")) return 6;
-    if (!strcmp(e, "ldg8")) return 9;
-    if (!strcmp(e, "dbg_noload")) return 7;
-    if (!strcmp(e, "dbg_noload128")) return 8;
+    if (!strcmp(e, "m128")) return 1;
+    if (!strcmp(e, "dbg_nomma")) return 2;
+    if (!strcmp(e, "dbg_nogather")) return 3;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
-  auto launch = [&](auto kern, int gw) -> int {
+  auto launch = [&](auto kern, int ks, int gw) -> int {
+    const SmemLayout L = smem_layout(pk->V, ks);
     HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(map, X, ldx, prm);
+    kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(X, ldx, prm);
     return HINM_OK;
   };
+  const bool m64 = pk->V <= 64 && variant != 1;
+  const int ks = env_ks == 64 || env_ks == 128 ? env_ks : (pk->V <= 64 ? 128 : 64);
+  const int gw = env_gw == 8 || env_gw == 16 ? env_gw : 8;
   int rc;
-  switch (variant) {
-    case 1: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8>, 8); break;
-    case 2: rc = launch(k_hinm_spmm<GATHER_TMA, 2>, 2); break;
-    case 3: rc = launch(k_hinm_spmm<GATHER_TMA, 4>, 4); break;
-    case 4: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 1>, 8); break;
-    case 5: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 2>, 8); break;
-    case 6: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8); break;  // M=128 for any V
-    case 7: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, true>, 8); break;
-    case 8: rc = launch(k_hinm_spmm<GATHER_CPASYNC, 8, 3, false>, 8); break;
-    case 9: rc = launch(k_hinm_spmm<GATHER_LDG, 8, 0, true>, 8); break;
-    default:
-      rc = pk->V <= 64 ? launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, true>, 8)
-                       : launch(k_hinm_spmm<GATHER_CPASYNC, 8, 0, false>, 8);
-      break;
+  if (variant == 2) {
+    rc = launch(k_hinm_spmm<128, 8, 1, true>, 128, 8);
+  } else if (variant == 3) {
+    rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8);
+  } else if (ks == 128) {
+    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true>, 128, 8) : launch(k_hinm_spmm<128, 8, 0, false>, 128, 8))
+                 : (m64 ? launch(k_hinm_spmm<128, 16, 0, true>, 128, 16) : launch(k_hinm_spmm<128, 16, 0, false>, 128, 16));
+  } else {
+    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<64, 8, 0, true>, 64, 8) : launch(k_hinm_spmm<64, 8, 0, false>, 64, 8))
+                 : (m64 ? launch(k_hinm_spmm<64, 16, 0, true>, 64, 16) : launch(k_hinm_spmm<64, 16, 0, false>, 64, 16));
   }
   if (rc) return rc;
   HINM_LAUNCH_CHECK();
