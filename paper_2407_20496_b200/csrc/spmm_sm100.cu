@@ -64,18 +64,20 @@ struct SmemLayout {
   uint32_t a, e, bar, tmem, total, ast;
 };
 
-// The A / metadata ring is decoupled from the gathered-X ring and deeper: its bulk copies see a
-// much longer latency than the cp.async gather under load, and with a shared barrier they held
-// every X stage hostage (scripts/l2_ring.cu).  Depth = whatever fits next to the X ring.
-__host__ __device__ inline SmemLayout smem_layout(int V, int KS) {
+// The A / metadata ring has its own barriers: its bulk copies see a much longer latency than the
+// cp.async gather under load, and with a shared barrier they held every X stage hostage
+// (scripts/l2_ring.cu).  One A stage covers one X stage (KS logical K: V*KS bytes of compressed
+// values + one metadata slot); depth = whatever fits next to the X ring.
+__host__ __device__ inline SmemLayout smem_layout(int V, int KS, bool m64) {
   SmemLayout L;
-  const uint32_t budget = 227 * 1024 - 1024 - 4096 - 512;
-  const uint32_t per = V * 64 + E_STAGE;
+  const uint32_t slack = m64 ? 0 : 4096;       // M=128 descriptor over-read past V rows
+  const uint32_t budget = 227 * 1024 - 1024 - 512 - slack;
+  const uint32_t per = V * KS + E_STAGE;
   const uint32_t xring = b_stages(KS) * b_stage_bytes(KS);
   const uint32_t fit = (budget - xring) / per;
   L.ast = fit < (uint32_t)MAX_ASTAGES ? fit : MAX_ASTAGES;
   L.a = xring;
-  L.e = L.a + L.ast * V * 64 + 4096;           // 4 KB slack: M=128 descriptor over-read
+  L.e = L.a + L.ast * V * KS + slack;
   L.bar = L.e + L.ast * E_STAGE;
   L.tmem = L.bar + (2 * 5 + 2 * MAX_ASTAGES + 2) * 8;
   L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const SmemLayout L = smem_layout(p.V, KS);
+  const SmemLayout L = smem_layout(p.V, KS, M64);
   const int V = p.V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
@@ -333,20 +335,21 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     int aslot = 0;
     uint32_t aphase = 0;
     UnitParams nxt = unit_params(p, blockIdx.x);
-    const uint32_t a_bytes = V * 64;
+    const uint32_t a_slot = V * KS;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const UnitParams cur = nxt;
       nxt = unit_params(p, u + gridDim.x);
-      const int nst = cur.kp / BK;
+      const int nst = cur.kp / BK;                         // 64-K steps of the unit
       const uint16_t* asrc = p.a_vals + (int64_t)cur.k0 * V / 2;
       const uint32_t* esrc0 = p.a_meta + (int64_t)cur.e0 * V * 4;
-      for (int s = 0; s < nst; ++s) {
+      for (int s = 0; s < nst; s += KS / BK) {             // one A stage per X stage
         mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
         const uint32_t fb = bar_afull + 8 * aslot;
         if (elect_one()) {
-          const uint32_t e_bytes = (s & 1) ? 0 : V * 16;
+          const uint32_t a_bytes = V * 64 * min(KS / BK, nst - s);
+          const uint32_t e_bytes = (s & 1) ? 0 : V * 16;   // metadata per 128-K block
           mbar_expect_tx(fb, a_bytes + e_bytes);
-          bulk_g2s(sA + aslot * a_bytes, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
+          bulk_g2s(sA + aslot * a_slot, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
           if (e_bytes) {
             const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
             if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
@@ -388,7 +391,9 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       ps = 0;
     };
     next_unit();
-    int r_row[PF], r_col[PF], r_n[PF];
+    const uint32_t ldx2 = (uint32_t)(ldx * 2);  // row pitch in bytes (host: < 2^32)
+    uint32_t r_row[PF];
+    int r_col[PF], r_n[PF];
     bool r_ok[PF];
     auto prefetch = [&](int slot) {
 #pragma unroll
@@ -400,7 +405,8 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         const int n = min(KS, pkp - ps * KS);
         r_n[j] = n;
         const int* gi = p.gidx + pk0 + ps * KS;
-        r_row[j] = lane < RPW && gw + lane * GW < n ? __ldg(gi + gw + lane * GW) : 0;
+        // raw row index: it is consumed PF stages later, so the load never stalls the warp here
+        r_row[j] = lane < RPW && gw + lane * GW < n ? (uint32_t)__ldg(gi + gw + lane * GW) : 0u;
         if (++ps * KS >= pkp) {
           pu += gridDim.x;
           pt += dt;
@@ -415,7 +421,6 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     // per-warp constant part of the SWIZZLE_128B destination (row r = gw + GW i: r & 7 = gw & 7)
     const uint32_t dst_lane = (lane >> 3) * (B_STAGE / 4) + gw * 128 + (((lane & 7) ^ (gw & 7)) << 4);
     const char* xbase = reinterpret_cast<const char*>(X);
-    const int64_t ldx2 = ldx * 2;
     int stage = 0;
     uint32_t phase = 0;
     bool done = false;
@@ -423,16 +428,20 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
 #pragma unroll
       for (int j = 0; j < PF; ++j) {
         if (!r_ok[j]) { done = true; break; }
+        // per row: SHFL + IMAD.WIDE + LDGSTS (the issue slots of the gather warps are the
+        // scarce resource, ncu source view); rows < 64 always exist, the rest only in full stages
         const int tok = r_col[j] + lane * 8;
         const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-        const char* xs = xbase + (src_bytes ? (int64_t)tok * 2 : 0);
-        const int my_row = r_row[j], n = r_n[j];
+        const char* xs = xbase + (src_bytes ? tok * 2 : 0);
+        const uint32_t my_row = r_row[j];
+        const bool full = r_n[j] == KS;
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int row = __shfl_sync(0xffffffffu, my_row, i);
-          if (DBG != 2 && gw + i * GW < n) cp_async_16(dst0 + i * GW * 128, xs + row * ldx2, src_bytes);
+          const uint32_t row = __shfl_sync(0xffffffffu, my_row, i);
+          if (DBG != 2 && (i * GW < 64 || full))
+            cp_async_16(dst0 + i * GW * 128, xs + (uint64_t)row * ldx2, src_bytes);  // IMAD.WIDE.U32
         }
         cp_async_arrive_noinc(bar_full + 8 * stage);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     const uint64_t a_desc0 = smem_desc(sA, 128, 256, 0);
     const uint64_t b_desc0 = smem_desc(sB, B_STAGE / 4, 1024, 2);
     const uint64_t e_desc0 = smem_desc(sE, 0, 128, 0);
-    const uint32_t a_step = (uint32_t)(V * 64) >> 4, a_half = (uint32_t)(32 * V) >> 4;
+    const uint32_t a_step = (uint32_t)(V * KS) >> 4, a_half = (uint32_t)(32 * V) >> 4;
     int stage = 0, aslot = 0;
     uint32_t phase = 0, aphase = 0, eslot = 0, acc_uses = 0;
     UnitParams nxt = unit_params(p, blockIdx.x);
@@ -463,31 +472,36 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       ++acc_uses;
       tc_fence_after();
       const int nst = kp / BK;
-      constexpr int SUB = KS / BK;  // A stages per X stage
-      for (int s = 0; s < nst; ++s) {
-        const int sub = s % SUB;
+      // one iteration per X stage (SUB = 1 or 2 A stages): all waits first, then one elected
+      // block issues the metadata copy, 2 * SUB MMAs and the commits (the issue loop, not the
+      // tensor pipe, was the MMA warp's limiter: ncu source view)
+      constexpr int SUB = KS / BK;
+      for (int s0 = 0; s0 < nst; s0 += SUB) {
+        const bool two = SUB == 2 && s0 + 1 < nst;
+        mbar_wait(bar_full + 8 * stage, phase);
         mbar_wait(bar_afull + 8 * aslot, aphase);
-        if (sub == 0) mbar_wait(bar_full + 8 * stage, phase);
         tc_fence_after();
         if (elect_one()) {
-          if ((s & 1) == 0) {
+          if ((s0 & 1) == 0) {  // metadata of the 128-K block starting at this step
             eslot = (eslot + 1) & (E_SLOTS - 1);
             tmem_cp_128x128b(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((aslot * E_STAGE) >> 4));
           }
-          const uint32_t ecol = tmem + E_COL + eslot * 4 + (s & 1) * 2;
+          const uint32_t ecol = tmem + E_COL + eslot * 4 + (s0 & 1) * 2;
           const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
-          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE + sub * BK * 128) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
           if (DBG != 1) {
-            mma_sp(tmem, ad, bd, idesc, ecol, s ? 1u : 0u);                       // id2 = 0
-            mma_sp(tmem, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);    // id2 = 1
+            mma_sp(tmem, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
+            mma_sp(tmem, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
+            if (two) {
+              mma_sp(tmem, ad + 2 * a_half, bd + (8192 >> 4), idesc, ecol + 2, 1u);
+              mma_sp(tmem, ad + 3 * a_half, bd + (12288 >> 4), idesc | 1u, ecol + 2, 1u);
+            }
           }
-          if (sub == SUB - 1 || s == nst - 1) tc_commit(bar_empty + 8 * stage);
           tc_commit(bar_aempty + 8 * aslot);
+          tc_commit(bar_empty + 8 * stage);
         }
         __syncwarp();
-        if (sub == SUB - 1 || s == nst - 1) {
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
       if (elect_one()) tc_commit(bar_acc_full);
@@ -598,6 +612,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   if (!pk->gidx || !pk->a_vals || !pk->a_meta || !pk->tile_kofs) return HINM_ERR_VALUE;
   if (B < 0 || (B % 8) || (ldx % 8) || (ldy % 8) || ldx < B || ldy < B) return HINM_ERR_VALUE;
   if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15)) return HINM_ERR_VALUE;
+  if (ldx * 2 >= (int64_t)1 << 32) return HINM_ERR_UNSUPPORTED;  // 32-bit row pitch
   if (B == 0 || pk->m == 0) return HINM_OK;
   Params prm;
   prm.tile_kofs = pk->tile_kofs;
@@ -631,13 +646,13 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
+  const bool m64 = pk->V <= 64 && variant != 1;
   auto launch = [&](auto kern, int ks, int gw) -> int {
-    const SmemLayout L = smem_layout(pk->V, ks);
+    const SmemLayout L = smem_layout(pk->V, ks, m64);
     HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(X, ldx, prm);
     return HINM_OK;
   };
-  const bool m64 = pk->V <= 64 && variant != 1;
   const int ks = env_ks == 64 || env_ks == 128 ? env_ks : (pk->V <= 64 ? 128 : 64);
   const int gw = env_gw == 8 || env_gw == 16 ? env_gw : 8;
   int rc;
