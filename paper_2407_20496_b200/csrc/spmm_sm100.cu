@@ -199,23 +199,25 @@ __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc)
 
 // 16 lanes x (32 + 32) columns: thread l < 16 gets lane l, columns c..c+31; thread l >= 16 gets
 // lane l-16, columns c+128..c+159.
+template <bool WAIT = true>
 __device__ __forceinline__ void tmem_ld_16x32bx2_x32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {"
       "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 128;"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  if (WAIT) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 // 32 lanes x 32 columns: thread l gets lane l, columns c..c+31.
+template <bool WAIT = true>
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {"
       "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  if (WAIT) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
@@ -558,19 +560,26 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         mbar_wait(bar_acc_full, ucount & 1);
         ++ucount;
         tc_fence_after();
-        uint32_t v[32];
+        // chunks are loaded in pairs (two tcgen05.ld in flight, one wait); the accumulator is
+        // released after the last pair's wait
+        uint32_t v0[32], v1[32];
 #pragma unroll 1
-        for (int c = 0; c < NCH; ++c) {
-          if (M64)
-            tmem_ld_16x32bx2_x32(t_row + c * 32, v);
-          else
-            tmem_ld_32x32b_x32(t_row + c * 32, v);
-          if (c == NCH - 1) {
+        for (int c = 0; c < NCH; c += 2) {
+          if (M64) {
+            tmem_ld_16x32bx2_x32<false>(t_row + c * 32, v0);
+            tmem_ld_16x32bx2_x32<false>(t_row + c * 32 + 32, v1);
+          } else {
+            tmem_ld_32x32b_x32<false>(t_row + c * 32, v0);
+            tmem_ld_32x32b_x32<false>(t_row + c * 32 + 32, v1);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c + 2 == NCH) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_acc_empty);
           }
-          store32(yrow, col_base + c * 32, v);
+          store32(yrow, col_base + c * 32, v0);
+          store32(yrow, col_base + c * 32 + 32, v1);
         }
       }
     }
