@@ -57,56 +57,63 @@ def sparse_flops(tokens):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every 5 ms while the timed region runs
+    (a background thread; nvidia-smi's 100 ms floor is longer than the timed region).  Falls back
+    to nvidia-smi when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,power.draw")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.proc = None
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            masks = [(n, getattr(pynvml, a)) for n, a in self.REASONS if hasattr(pynvml, a)]
+        except Exception:  # pragma: no cover - no NVML on this host
+            return self
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((mhz, [n for n, m in masks if r & m]))
+                except Exception:
+                    pass
+                self._stop.wait(self.period)
+
+        self._thread = threading.Thread(target=loop, daemon=True)
+        self._thread.start()
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = sorted({n for _, rs in self.samples for n in rs})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 5 ms"}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -227,6 +234,17 @@ def run_ours(args):
     p_sparse = 2.0 * pk["bf16_tflops"]
     f_sp = sparse_flops(GLOBAL_TOKENS // world)
     achieved = f_sp / (sum(per_kernel.values()) * 1e-3) / 1e12
+    # the gather roofline: every kept K-row of a tile is streamed L2 -> SMEM once per 256-token
+    # block (2 * T * k_bar * tokens bytes) plus the compressed A / metadata image per unit
+    gathered = sum(2.0 * (m // V) * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
+    a_image = sum((m // V) * int(n * (1 - SV)) * V * 1.125 * -(-tokens // 256) for _, m, n in layer_shapes())
+    l2_tbs = (gathered + a_image) / (sum(per_kernel.values()) * 1e-3) / 1e12
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "spmm_dram_traffic.json")))
+        traffic = tr["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        tr = None
     comp_bytes = 0
     for name, m, n in layer_shapes():
         kbar = int(n * (1 - SV))
@@ -256,9 +274,15 @@ def run_ours(args):
                               "per_gemm_ms": {k: round(v, 4) for k, v in cublas.items()}},
         "per_spmm_ms": {k: round(v, 4) for k, v in per_kernel.items()},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(p_sparse, 1),
-                     "unit": "TFLOP/s", "frac": round(achieved / p_sparse, 4), "traffic": None,
+                     "unit": "TFLOP/s", "frac": round(achieved / p_sparse, 4), "traffic": traffic,
                      "peak_source": f"2 x bf16_tflops of {kind} MEASURED_PEAKS.json (2:4 sparse)",
-                     "algorithmic": "2*m*k_bar*tokens per SpMM (k_bar = n/2 kept vectors)"},
+                     "algorithmic": "2*m*k_bar*tokens per SpMM (k_bar = n/2 kept vectors)",
+                     "traffic_note": (tr or {}).get("note"),
+                     "binding": {"resource": "L2->SMEM gather (cp.async)",
+                                 "achieved_tbs": round(l2_tbs, 2), "cap_tbs": 21.2,
+                                 "frac": round(l2_tbs / 21.2, 3),
+                                 "cap_source": "scripts/l2_ring.cu on B200: 16 warps x 128-row stages, "
+                                               "no MMA (profiles/r01_gather_microbench.txt)"}},
         "compressor": {"ms": {k: round(v, 3) for k, v in comp_ms.items()},
                        "algorithmic_bytes": comp_bytes,
                        "gbs": round(comp_bytes / (sum(comp_ms.values()) * 1e-3) / 1e9, 1),
@@ -278,8 +302,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(pack, tokens: int):
-    """Oracle port of hinm_spmm (float64 gather + GEMV, host BLAS) on a bounded token sample."""
+def cpu_baseline(pack, tokens: int, min_seconds: float = 10.0):
+    """Oracle port of hinm_spmm (float64 gather + GEMV, host BLAS) on a bounded token sample,
+    repeated until about min_seconds of CPU work have been timed."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import hinm_oracle as O
 
@@ -291,14 +316,19 @@ def cpu_baseline(pack, tokens: int):
     tiles = pack.to_host_tiles()
     rng = np.random.default_rng(1)
     X = rng.standard_normal((pack.n, tokens)).astype(np.float32).astype(np.float64)
-    t0 = time.perf_counter()
-    Y = O.hinm_spmm(tiles, X, pack.m, pack.V, pack.N, pack.M)
-    O.restore_row_order(Y, pack.sigma_o.cpu().numpy())
-    dt = time.perf_counter() - t0
-    f = 2.0 * pack.m * pack.n * tokens
+    so = pack.sigma_o.cpu().numpy()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        Y = O.hinm_spmm(tiles, X, pack.m, pack.V, pack.N, pack.M)
+        O.restore_row_order(Y, so)
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            break
+    f = 2.0 * pack.m * pack.n * tokens * reps
     return {"value": round(f / dt / 1e12, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
             "kind": "port", "seconds": round(dt, 2),
-            "sample": f"down projection 4096x11008 (V=64 2:4), {tokens} tokens, oracle "
+            "sample": f"down projection 4096x11008 (V=64 2:4), {reps} x {tokens} tokens, oracle "
                       f"hinm_spmm + restore_row_order, float64; host cpu_count={os.cpu_count()}"}
 
 
