@@ -136,6 +136,34 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// L2 eviction-priority policies.  The compressed A / metadata image of every tile is re-read once
+// per token block and must survive the streaming Y stores: A loads are evict_last, Y stores
+// evict_first (run-to-run variance of the 4096x11008 layer came from A being evicted).
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_global_v4_hint(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -338,6 +366,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     uint32_t aphase = 0;
     UnitParams nxt = unit_params(p, blockIdx.x);
     const uint32_t a_slot = V * KS;
+    const uint64_t pol_a = l2_policy_evict_last();
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const UnitParams cur = nxt;
       nxt = unit_params(p, u + gridDim.x);
@@ -351,14 +380,14 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const uint32_t a_bytes = V * 64 * min(KS / BK, nst - s);
           const uint32_t e_bytes = (s & 1) ? 0 : V * 16;   // metadata per 128-K block
           mbar_expect_tx(fb, a_bytes + e_bytes);
-          bulk_g2s(sA + aslot * a_slot, asrc + (int64_t)s * BK * V / 2, a_bytes, fb);
+          bulk_g2s_hint(sA + aslot * a_slot, asrc + (int64_t)s * BK * V / 2, a_bytes, fb, pol_a);
           if (e_bytes) {
             const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
             if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
               for (int q = 0; q < V / 16; ++q)
-                bulk_g2s(sE + aslot * E_STAGE + q * 512, esrc + q * 64, 256, fb);
+                bulk_g2s_hint(sE + aslot * E_STAGE + q * 512, esrc + q * 64, 256, fb, pol_a);
             } else {
-              bulk_g2s(sE + aslot * E_STAGE, esrc, e_bytes, fb);
+              bulk_g2s_hint(sE + aslot * E_STAGE, esrc, e_bytes, fb, pol_a);
             }
           }
         }
@@ -529,6 +558,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
       };
       // 32 accumulator columns (fp32 bits) -> bf16 -> 4 x 16-byte stores of one row segment
+      const uint64_t pol_y = l2_policy_evict_first();
       auto store32 = [&](uint16_t* yrow, int col, const uint32_t (&v)[32]) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -538,7 +568,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
             o.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
             o.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
             o.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
-            *reinterpret_cast<uint4*>(yrow + col + j * 8) = o;
+            st_global_v4_hint(yrow + col + j * 8, o, pol_y);
           }
         }
       };

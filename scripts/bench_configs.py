@@ -1,0 +1,134 @@
+"""Every BASELINE.json configuration on one B200: HiNM SpMM vs cuBLAS
+dense bf16 on the same shapes, plus the GPU compressor time.  One JSON document on stdout.
+
+    python scripts/bench_configs.py [--quick] > profiles/r01_configs.json
+
+Timing: CUDA events around ITERS back-to-back launches after 3 warm-ups; inputs are resident in
+HBM.  Effective TFLOP/s = 2*m*n*tokens / t (the BASELINE.json metric).  Synthetic N(0,1) bf16
+weights / activations, random sigma_o (seeded).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2407_20496_b200 as H  # noqa: E402
+
+DEV = torch.device("cuda")
+
+
+def timed(fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def gemm_case(m, n, tokens, V, sv, seed, iters, cublas_cache=None):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    W = torch.randn(m, n, generator=g, device=DEV).to(torch.bfloat16)
+    X = torch.randn(n, tokens, generator=g, device=DEV).to(torch.bfloat16)
+    Y = torch.empty(m, tokens, dtype=torch.bfloat16, device=DEV)
+    so = np.random.default_rng(seed).permutation(m)
+    cfg = H.HiNMConfig(V, 2, 4, sv)
+    H.compress(W, cfg, so)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pack = H.compress(W, cfg, so)
+    torch.cuda.synchronize()
+    comp_ms = (time.perf_counter() - t0) * 1e3
+    ms = timed(lambda: H.spmm(pack, X, out=Y, order="original"), iters)
+    key = (m, n, tokens)
+    if cublas_cache is not None and key in cublas_cache:
+        cb = cublas_cache[key]
+    else:
+        cb = timed(lambda: torch.matmul(W, X), iters)
+        if cublas_cache is not None:
+            cublas_cache[key] = cb
+    f = 2.0 * m * n * tokens
+    return {"m": m, "n": n, "tokens": tokens, "V": V, "s_v": sv, "spmm_ms": round(ms, 4),
+            "cublas_ms": round(cb, 4), "speedup": round(cb / ms, 3),
+            "eff_tflops": round(f / ms / 1e9, 1), "cublas_tflops": round(f / cb / 1e9, 1),
+            "compress_ms": round(comp_ms, 3)}
+
+
+def summarize(rows, label):
+    sp = sum(r["spmm_ms"] * r.get("count", 1) for r in rows)
+    cb = sum(r["cublas_ms"] * r.get("count", 1) for r in rows)
+    fl = sum(2.0 * r["m"] * r["n"] * r["tokens"] * r.get("count", 1) for r in rows)
+    return {"config": label, "spmm_ms_total": round(sp, 3), "cublas_ms_total": round(cb, 3),
+            "speedup": round(cb / sp, 3), "eff_tflops": round(fl / sp / 1e9, 1)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    it = 5 if args.quick else 20
+    out = {"device": torch.cuda.get_device_name(), "iters": it}
+    cache = {}
+
+    # cfg1: BERT-base FFN 768x3072 (and the transposed reading 3072x768), 512 tokens
+    rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache), gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache)]
+    out["cfg1"] = {"rows": rows, "note": "launch/latency bound (2.4 GFLOP); the CPU reference path "
+                   "for this config is bench.py --impl reference / cpu_baseline"}
+
+    # cfg2: BERT-base, 12 layers x (Q, K, V, O 768x768; FFN1 3072x768; FFN2 768x3072), 4096 tokens
+    rows = []
+    for nm, m, n, cnt in (("qkvo", 768, 768, 48), ("ffn1", 3072, 768, 12), ("ffn2", 768, 3072, 12)):
+        r = gemm_case(m, n, 4096, 64, 0.5, 11, it, cache)
+        r.update({"layer": nm, "count": cnt})
+        rows.append(r)
+    out["cfg2"] = {"rows": rows, "total": summarize(rows, "cfg2 BERT-base 72 GEMMs, 32x128 tokens")}
+
+    # cfg3: LLaMA-7B FFN, 2048..16384 tokens
+    rows = []
+    for tok in (2048, 4096, 8192, 16384):
+        for nm, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
+            r = gemm_case(m, n, tok, 64, 0.5, 21, it, cache)
+            r["layer"] = nm
+            rows.append(r)
+    out["cfg3"] = {"rows": rows}
+
+    # cfg4: ResNet-50 im2col GEMMs, batch 256; conv1 (64x147) stays dense
+    shapes = [(64, 64, 802816, 1), (64, 576, 802816, 3), (256, 64, 802816, 4), (64, 256, 802816, 2),
+              (128, 256, 802816, 1), (128, 1152, 200704, 4), (512, 128, 200704, 4),
+              (512, 256, 200704, 1), (128, 512, 200704, 3), (256, 512, 200704, 1),
+              (256, 2304, 50176, 6), (1024, 256, 50176, 6), (1024, 512, 50176, 1),
+              (256, 1024, 50176, 5), (512, 1024, 50176, 1), (512, 4608, 12544, 3),
+              (2048, 512, 12544, 3), (2048, 1024, 12544, 1), (512, 2048, 12544, 2)]
+    for sv, lab in ((0.5, "75%"), (0.75, "87.5%")):
+        rows = []
+        for m, n, tok, cnt in shapes:
+            if (n * (1 - sv)) % 4:
+                continue
+            r = gemm_case(m, n, tok, 64, sv, 31, max(3, it // 4), cache)
+            r["count"] = cnt
+            rows.append(r)
+        out[f"cfg4_{lab}"] = {"rows": rows, "total": summarize(rows, f"cfg4 ResNet-50 im2col {lab}")}
+
+    # cfg5: 4096x4096, V in {32, 64, 128} x vector-keep {50%, 25%}, 16384 tokens
+    rows = []
+    for V in (32, 64, 128):
+        for sv in (0.5, 0.75):
+            rows.append(gemm_case(4096, 4096, 16384, V, sv, 41, it, cache))
+    out["cfg5"] = {"rows": rows}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
