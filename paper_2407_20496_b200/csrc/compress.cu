@@ -53,56 +53,45 @@ __global__ void k_scores(Src src, const int32_t* __restrict__ sigma_o, int n, in
   scores[(int64_t)t * n + j] = acc + 0.0;  // canonicalise -0.0 (only compared, never emitted)
 }
 
-// a3 (bf16 fast path, n % 8 == 0): 8 consecutive columns per thread (one 16-byte load per
-// row), independent fp64 chains per column, still summed sequentially in sigma_o row order.
+// a3 (bf16 fast path, n % 4 == 0): 4 consecutive columns per thread (one 8-byte load per row;
+// a warp reads 256 contiguous bytes of a row), independent fp64 chains per column, still summed
+// sequentially in sigma_o row order.  Rows are loaded 8 at a time ahead of the adds so that
+// each thread keeps 8 loads in flight (the kernel is an HBM stream over W).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, int64_t ldw,
+__global__ void __launch_bounds__(NT) k_scores4(const uint16_t* __restrict__ W, int64_t ldw,
                                                 const int32_t* __restrict__ sigma_o, int n, int V,
                                                 double* __restrict__ scores) {
   extern __shared__ int32_t s_rows[];
   const int t = blockIdx.y;
   for (int r = threadIdx.x; r < V; r += NT) s_rows[r] = sigma_o[(int64_t)t * V + r];
   __syncthreads();
-  const int j0 = (blockIdx.x * NT + threadIdx.x) * 8;
+  const int j0 = (blockIdx.x * NT + threadIdx.x) * 4;
   if (j0 >= n) return;
-  double acc[8];
-  {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[0] * ldw + j0));
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  const uint16_t* Wc = W + j0;
+  double acc[4];
+  auto add = [&](uint2 v, bool first) {
+    const uint32_t w[2] = {v.x, v.y};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      acc[2 * k] = bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
-      acc[2 * k + 1] = bf16_abs_f64((uint16_t)(w[k] >> 16));
+    for (int k = 0; k < 2; ++k) {
+      const double lo = bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
+      const double hi = bf16_abs_f64((uint16_t)(w[k] >> 16));
+      acc[2 * k] = first ? lo : acc[2 * k] + lo;
+      acc[2 * k + 1] = first ? hi : acc[2 * k + 1] + hi;
     }
+  };
+  int r = 0;
+  for (; r + 8 <= V; r += 8) {
+    uint2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = __ldg(reinterpret_cast<const uint2*>(Wc + (int64_t)s_rows[r + u] * ldw));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add(v[u], r + u == 0);
   }
-  int r = 1;
-  for (; r + 4 <= V; r += 4) {
-    uint4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      v[u] = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[r + u] * ldw + j0));
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[2 * k] = acc[2 * k] + bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
-        acc[2 * k + 1] = acc[2 * k + 1] + bf16_abs_f64((uint16_t)(w[k] >> 16));
-      }
-    }
-  }
-  for (; r < V; ++r) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(W + (int64_t)s_rows[r] * ldw + j0));
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      acc[2 * k] = acc[2 * k] + bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
-      acc[2 * k + 1] = acc[2 * k + 1] + bf16_abs_f64((uint16_t)(w[k] >> 16));
-    }
-  }
+  for (; r < V; ++r) add(__ldg(reinterpret_cast<const uint2*>(Wc + (int64_t)s_rows[r] * ldw)), r == 0);
   double* out = scores + (int64_t)t * n + j0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) out[k] = acc[k] + 0.0;
+  for (int k = 0; k < 4; ++k) out[k] = acc[k] + 0.0;
 }
 
 __global__ void k_iota_cols(int32_t* __restrict__ v, int n, int64_t total) {
@@ -116,14 +105,30 @@ __global__ void k_segment_offsets(int32_t* __restrict__ off, int T, int n) {
 }
 
 // a4: gains of consecutive M-chunks of the sorted scores (numpy pairwise over the chunk).
+// Also accumulates the OR / AND of all budget keys (keybits[0] |=, keybits[1] &=) so that the
+// radix select skips the bytes on which every key agrees.
+__device__ __forceinline__ uint64_t gain_key(double g);
 __global__ void k_gains(const double* __restrict__ sorted, int n, int M, int G, int T,
-                        double* __restrict__ gains) {
+                        double* __restrict__ gains, unsigned long long* __restrict__ keybits) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)T * G) return;
-  const int t = (int)(i / G), q = (int)(i % G);
-  const double* base = sorted + (int64_t)t * n + (int64_t)q * M;
-  auto get = [&](int64_t k) { return base[k]; };
-  gains[i] = np_pairwise_sum(get, 0, M) + 0.0;
+  uint64_t kor = 0, kand = ~0ull;
+  if (i < (int64_t)T * G) {
+    const int t = (int)(i / G), q = (int)(i % G);
+    const double* base = sorted + (int64_t)t * n + (int64_t)q * M;
+    auto get = [&](int64_t k) { return base[k]; };
+    const double g = np_pairwise_sum(get, 0, M) + 0.0;
+    gains[i] = g;
+    kor = kand = gain_key(g);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+    kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(keybits, (unsigned long long)kor);
+    atomicAnd(keybits + 1, (unsigned long long)kand);
+  }
 }
 
 // Orderable key: ascending key <=> descending gain (gains are >= +0.0 after canonicalisation).
@@ -141,6 +146,37 @@ __device__ int row_bound(const double* row, int G, uint64_t x, bool upper) {
     if (go_right) lo = mid + 1; else hi = mid;
   }
   return lo;
+}
+
+// Warp-cooperative version (all 32 lanes call it with the same arguments): a 32-ary search, so
+// ~log32(G) dependent load rounds instead of log2(G).  Returns the bound in every lane.
+__device__ int row_bound_warp(const double* row, int G, uint64_t x, bool upper) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = G;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int p = lo + lane * step;  // probe positions lo, lo+step, ...
+    bool right = false;
+    if (p < hi) {
+      const uint64_t k = gain_key(row[p]);
+      right = upper ? (k <= x) : (k < x);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, right);  // prefix of lanes (keys non-decreasing)
+    const int c = __popc(m);
+    // positions < lo + c*step satisfy the predicate except possibly inside the last step
+    const int nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+    const int nhi = min(hi, lo + c * step);
+    lo = nlo;
+    hi = max(nhi, nlo);
+  }
+  // final linear pass over at most 32 positions
+  const int p = lo + lane;
+  bool right = false;
+  if (p < hi) {
+    const uint64_t k = gain_key(row[p]);
+    right = upper ? (k <= x) : (k < x);
+  }
+  return lo + __popc(__ballot_sync(0xffffffffu, right));
 }
 
 template <int NT>
@@ -248,30 +284,58 @@ __global__ void __launch_bounds__(NT) k_budget(const double* __restrict__ gains,
 
 // a4 (fast path, n <= 16384): one CTA per tile sorts the tile's scores in registers/smem with a
 // stable block radix sort (descending keys; input in column order => ties keep the lower
-// column first, == np.lexsort((cols, -score))).
+// column first, == np.lexsort((cols, -score))).  Scores are >= +0.0, so their IEEE bit patterns
+// order like the values; only the bits that differ inside the tile are sorted (column sums of
+// bf16 magnitudes share their top exponent bits and end in long runs of zero mantissa bits:
+// ~32 of 64 bits vary on N(0,1) weights, 6 radix passes instead of 11).
+struct OrOp {
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const { return a | b; }
+};
+struct AndOp {
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const { return a & b; }
+};
+
 template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_tile_sort(const double* __restrict__ scores, int n,
                                                   double* __restrict__ sorted,
                                                   int32_t* __restrict__ order) {
-  typedef cub::BlockRadixSort<double, NT, ITEMS, int32_t, 6> BRS;
+  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS, int32_t, 6> BRS;
+  typedef cub::BlockReduce<uint64_t, NT> BR;
   extern __shared__ __align__(16) uint8_t sort_smem[];
   typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(sort_smem);
+  __shared__ typename BR::TempStorage red_tmp;
+  __shared__ uint64_t s_or, s_and;
   const int t = blockIdx.x;
   const double* row = scores + (int64_t)t * n;
-  double keys[ITEMS];
+  uint64_t keys[ITEMS];
   int32_t vals[ITEMS];
+  uint64_t lor = 0, land = ~0ull;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int j = threadIdx.x * ITEMS + i;  // blocked arrangement = column order
-    keys[i] = j < n ? row[j] : -INFINITY;
+    keys[i] = j < n ? (uint64_t)__double_as_longlong(row[j]) : 0ull;
     vals[i] = j;
+    if (j < n) { lor |= keys[i]; land &= keys[i]; }
   }
-  BRS(tmp).SortDescending(keys, vals);
+  lor = BR(red_tmp).Reduce(lor, OrOp());
+  if (threadIdx.x == 0) s_or = lor;
+  __syncthreads();
+  land = BR(red_tmp).Reduce(land, AndOp());
+  if (threadIdx.x == 0) s_and = land;
+  __syncthreads();
+  const uint64_t diff = s_or ^ s_and;  // bits that differ between some keys of the tile
+  if (diff) {
+    const int begin = __ffsll((long long)diff) - 1, end = 64 - __clzll((long long)diff);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (threadIdx.x * ITEMS + i >= n) keys[i] = s_and;  // padding: minimum key, after ties
+    BRS(tmp).SortDescending(keys, vals, begin, end);
+  }
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int j = threadIdx.x * ITEMS + i;
     if (j < n) {
-      sorted[(int64_t)t * n + j] = keys[i];
+      sorted[(int64_t)t * n + j] = __longlong_as_double((long long)keys[i]);
       order[(int64_t)t * n + j] = vals[i];
     }
   }
@@ -285,18 +349,39 @@ __device__ void budget_tail(const double* __restrict__ gains, int T, int G, int6
                             int32_t* __restrict__ hi_scr, int32_t* __restrict__ tile_ptr) {
   __shared__ int64_t red;
   int64_t less = 0;
+  int64_t qmin = G, qmax = 0;  // chunk range holding keys equal to xs (ties)
   for (int t = threadIdx.x; t < T; t += NT) {
     if (compute_bounds) {
       const double* row = gains + (int64_t)t * G;
       lo_scr[t] = row_bound(row, G, xs, false);
       hi_scr[t] = row_bound(row, G, xs, true);
     }
-    less += lo_scr[t];
+    const int l = lo_scr[t], h = hi_scr[t];
+    less += l;
+    if (h > l) {
+      qmin = min(qmin, (int64_t)l);
+      qmax = max(qmax, (int64_t)h - 1);
+    }
   }
   __syncthreads();
   less = block_sum64<NT>(less, &red);
+  {
+    typedef cub::BlockReduce<int64_t, NT> BRm;
+    __shared__ typename BRm::TempStorage mtmp;
+    __shared__ int64_t s_qmin, s_qmax;
+    const int64_t a = BRm(mtmp).Reduce(qmin, cub::Min());
+    if (threadIdx.x == 0) s_qmin = a;
+    __syncthreads();
+    const int64_t b = BRm(mtmp).Reduce(qmax, cub::Max());
+    if (threadIdx.x == 0) s_qmax = b;
+    __syncthreads();
+    qmin = s_qmin;
+    qmax = s_qmax;
+  }
   const int64_t R = total_groups - less;
-  int qlo = 0, qhi = G - 1;
+  // the answer Q lies in [qmin, qmax]: F(Q) = 0 < R below it and F = #ties >= R at its top, so
+  // the search usually ends at once (a single tile holds the threshold key)
+  int qlo = (int)min(qmin, (int64_t)G - 1), qhi = (int)max((int64_t)qlo, min(qmax, (int64_t)G - 1));
   while (qlo < qhi) {
     int mid = (qlo + qhi) >> 1;
     int64_t f = 0;
@@ -420,6 +505,7 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ gains, int T, int G,
                                                     int64_t total_groups, int M,
+                                                    const unsigned long long* __restrict__ keybits,
                                                     uint32_t* __restrict__ ghist,
                                                     int32_t* __restrict__ lo_scr,
                                                     int32_t* __restrict__ hi_scr,
@@ -432,10 +518,15 @@ __global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ g
   __shared__ int64_t s_k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t total = (int64_t)T * G;
-  uint64_t prefix = 0, pmask = 0;
+  // bytes on which all keys agree need no pass: they are taken from the AND of the keys
+  const uint64_t kor = __ldcg(keybits), kand = __ldcg(keybits + 1), diff = kor ^ kand;
+  const int top = diff ? (63 - __clzll((long long)diff)) / 8 * 8 : -8;
+  const int bottom = diff ? (__ffsll((long long)diff) - 1) / 8 * 8 : 0;
+  const uint64_t above = top >= 56 ? 0ull : ~0ull << (top + 8);
+  uint64_t prefix = kand & above, pmask = above;
   int64_t k = total_groups;
   int pass = 0;
-  for (int shift = 56; shift >= 0; shift -= 8, ++pass) {
+  for (int shift = top; shift >= bottom; shift -= 8, ++pass) {
     for (int i = threadIdx.x; i < NW * 256; i += NT) (&hist[0][0])[i] = 0;
     __syncthreads();
     for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
@@ -487,10 +578,11 @@ __global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ g
     pmask |= (uint64_t)255 << shift;
     __syncthreads();
   }
-  for (int t = blockIdx.x * NT + threadIdx.x; t < T; t += gridDim.x * NT) {
+  prefix |= kand & ~pmask;  // constant low bytes
+  for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {  // one warp per tile
     const double* row = gains + (int64_t)t * G;
-    lo_scr[t] = row_bound(row, G, prefix, false);
-    hi_scr[t] = row_bound(row, G, prefix, true);
+    const int a = row_bound_warp(row, G, prefix, false), b = row_bound_warp(row, G, prefix, true);
+    if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
   }
   grid.sync();
   if (blockIdx.x != 0) return;
@@ -888,6 +980,128 @@ __global__ void k_pack_gidx(const int32_t* __restrict__ tile_ptr, const int32_t*
   }
 }
 
+
+// 2:4 select + pack, fused (fast path of hinm_compress_bf16 when the operand image is wanted).
+// One CTA per (tile, R consecutive rows).  Weight rows stream through a double-buffered smem row
+// (cp.async, one row ahead).  Per row and 16-K chunk (4 groups) one thread selects the top-2 of
+// each group (ties -> lower position, == the stable argsort of pruning.py:176) and writes
+//   reference view : kept (2 bf16 / group) + nm_pos (2 x u8 / group)      (pruning.py:305-318)
+//   operand image  : one 16-byte UMMA core-matrix row of a_vals and its 16 metadata bits (the
+//                    half m1 of word (block, lane m0 + 8*k1 + 16*m2, w): the two rows that share
+//                    a word write different halves, so no staging or atomics are needed)
+// Padding chunks (k_t .. kp) get zero values; positions {0, 1} fill the metadata up to the end
+// of the last 128-K block.  The CTA of rows 0.. also writes gidx.
+__device__ __forceinline__ void top2_of_4(uint16_t v0, uint16_t v1, uint16_t v2, uint16_t v3,
+                                          uint32_t& pos, uint32_t& vals) {
+  const uint32_t a0 = v0 & 0x7FFFu, a1 = v1 & 0x7FFFu, a2 = v2 & 0x7FFFu, a3 = v3 & 0x7FFFu;
+  const int r0 = (a1 > a0) + (a2 > a0) + (a3 > a0);
+  const int r1 = (a0 >= a1) + (a2 > a1) + (a3 > a1);
+  const int r2 = (a0 >= a2) + (a1 >= a2) + (a3 > a2);
+  int p0, p1;
+  uint16_t k0, k1;
+  if (r0 < 2) {
+    p0 = 0; k0 = v0;
+    if (r1 < 2) { p1 = 1; k1 = v1; } else if (r2 < 2) { p1 = 2; k1 = v2; } else { p1 = 3; k1 = v3; }
+  } else if (r1 < 2) {
+    p0 = 1; k0 = v1;
+    if (r2 < 2) { p1 = 2; k1 = v2; } else { p1 = 3; k1 = v3; }
+  } else {
+    p0 = 2; k0 = v2; p1 = 3; k1 = v3;
+  }
+  pos = (uint32_t)p0 | ((uint32_t)p1 << 8);
+  vals = (uint32_t)k0 | ((uint32_t)k1 << 16);
+}
+
+template <int NT, int R>
+__global__ void __launch_bounds__(NT) k_select_pack(
+    const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
+    const int32_t* __restrict__ sig_ptr, const int32_t* __restrict__ sig_idx, int n, int V,
+    const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
+    uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
+    uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
+  extern __shared__ __align__(16) uint8_t sp_smem[];
+  const int t = blockIdx.y, r0 = blockIdx.x * R;
+  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
+  const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
+  const int eofs = eofs_g[t], nblk = eofs_g[t + 1] - eofs;
+  if (kp == 0) return;
+  const size_t idx_bytes = ((size_t)kp * 4 + 15) & ~size_t(15);
+  const size_t row_bytes = ((size_t)n * 2 + 15) & ~size_t(15);
+  int32_t* s_idx = reinterpret_cast<int32_t*>(sp_smem);
+  uint8_t* s_rows = sp_smem + idx_bytes;
+  const bool vec_rows = (ldw & 7) == 0 && (n & 7) == 0 && ((uintptr_t)W & 15) == 0;
+  auto fetch_row = [&](int rr) {
+    const uint16_t* wrow = W + (int64_t)sigma_o[(int64_t)t * V + r0 + rr] * ldw;
+    uint16_t* dst = reinterpret_cast<uint16_t*>(s_rows + (rr & 1) * row_bytes);
+    if (vec_rows) {
+      for (int i = threadIdx.x; i < n / 8; i += NT) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + 8 * i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(wrow + 8 * i) : "memory");
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += NT) dst[i] = wrow[i];
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch_row(0);
+  // group column indices (padding entries repeat a valid column: their values are ignored)
+  for (int i = threadIdx.x; i < kp; i += NT) s_idx[i] = sig_idx[b + (i < k ? i : k - 1)];
+  if (r0 == 0)
+    for (int i = threadIdx.x; i < kp; i += NT) gidx[kofs + i] = sig_idx[b + (i < k ? i : k - 1)];
+  const int64_t ref_base = (int64_t)V * (b / 4) * 2;
+  const int nch = kp / 16;        // 16-K chunks with values
+  const int nch_meta = nblk * 8;  // chunks covered by metadata blocks (>= nch)
+  uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
+  for (int rr = 0; rr < R; ++rr) {
+    const int r = r0 + rr;
+    if (rr + 1 < R) {
+      fetch_row(rr + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(s_rows + (rr & 1) * row_bytes);
+    const int64_t rbase = ref_base + (int64_t)r * G * 2;
+    const int m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
+    for (int ch = threadIdx.x; ch < nch_meta; ch += NT) {
+      const int g0 = ch * 4;
+      uint32_t pos[4], val[4];
+      uint32_t bits = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int g = g0 + c;
+        if (g < G) {
+          const int4 c4 = reinterpret_cast<const int4*>(s_idx)[g];
+          top2_of_4(row[c4.x], row[c4.y], row[c4.z], row[c4.w], pos[c], val[c]);
+        } else {
+          pos[c] = 0x100u;  // positions {0, 1}, zero values
+          val[c] = 0u;
+        }
+        bits |= ((pos[c] & 3u) | (((pos[c] >> 8) & 3u) << 2)) << (4 * c);
+      }
+      if (g0 < G) {  // reference view (real groups only)
+        if (g0 + 3 < G && (rbase & 7) == 0) {  // 8 / 16-byte aligned (rows with G % 4 != 0 are not)
+          *reinterpret_cast<uint2*>(nm_pos + rbase + (int64_t)g0 * 2) =
+              make_uint2(pos[0] | (pos[1] << 16), pos[2] | (pos[3] << 16));
+          *reinterpret_cast<uint4*>(kept + rbase + (int64_t)g0 * 2) = make_uint4(val[0], val[1], val[2], val[3]);
+        } else {
+          for (int c = 0; c < 4 && g0 + c < G; ++c) {
+            reinterpret_cast<uint16_t*>(nm_pos + rbase)[g0 + c] = (uint16_t)pos[c];
+            reinterpret_cast<uint32_t*>(kept + rbase)[g0 + c] = val[c];
+          }
+        }
+      }
+      if (ch < nch)  // operand image: 8 compressed values = one 16-byte core-matrix row
+        *reinterpret_cast<uint4*>(a_vals + aval_offset(kofs, V, r, 2 * g0)) =
+            make_uint4(val[0], val[1], val[2], val[3]);
+      const int eb = g0 >> 5, w = (g0 >> 3) & 3, k1 = (g0 >> 2) & 1;
+      meta16[(((int64_t)eb * V + m0 + 8 * k1 + 16 * m2) * 4 + w) * 2 + m1] = (uint16_t)bits;
+    }
+    __syncthreads();  // row buffer (rr & 1) is refilled by the next iteration's fetch
+  }
+}
+
 }  // namespace hinm
 
 // ---------------------------------------------------------------------------------------------
@@ -929,7 +1143,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->hi = take(4 * T);
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
   L->err = take(16);
-  L->ghist = take(8 * 256 * 4);
+  L->ghist = take(8 * 256 * 4 + 16);  // radix histograms + key OR / AND words
   size_t cb = 0;
   int st = cub_sort_bytes((int)T, n, &cb);
   if (st) return st;
@@ -941,7 +1155,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
 template <int ITEMS>
 int launch_tile_sort_items(const double* scores, int n, int T, double* sorted, int32_t* order,
                            cudaStream_t stream) {
-  typedef cub::BlockRadixSort<double, 1024, ITEMS, int32_t, 6> BRS;
+  typedef cub::BlockRadixSort<uint64_t, 1024, ITEMS, int32_t, 6> BRS;
   const size_t smem = sizeof(typename BRS::TempStorage);
   if (smem > 48 * 1024)
     HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<1024, ITEMS>,
@@ -1018,8 +1232,8 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   double* gains = (double*)(ws + L.gains);
   Src src{W, ldw, Wd, ldwd, S, lds};
 
-  if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
-    k_scores8<128><<<dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream>>>(
+  if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
+    k_scores4<128><<<dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream>>>(
         W, ldw, sigma_o, n, V, scores);
   } else {
     k_scores<<<dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream>>>(src, sigma_o, n, V, scores);
@@ -1038,19 +1252,25 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     HINM_CUDA_TRY(cub::DeviceSegmentedRadixSort::SortPairsDescending(
         ws + L.cub, cb, scores, sorted, vals_in, order, Tn, T, offsets, offsets + 1, 0, 64, stream));
   }
+  uint32_t* ghist = (uint32_t*)(ws + L.ghist);
+  unsigned long long* keybits = (unsigned long long*)(ghist + 8 * 256);
+  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4 + 8, stream));
+  HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
   if (G > 0) {
-    k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains);
+    k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains,
+                                                                         keybits);
     HINM_LAUNCH_CHECK();
   }
   {
-    uint32_t* ghist = (uint32_t*)(ws + L.ghist);
     int32_t* lo_s = (int32_t*)(ws + L.lo);
     int32_t* hi_s = (int32_t*)(ws + L.hi);
-    HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4, stream));
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_budget_coop<1024>, 1024, 0);
+    static int per_sm = -1, sms = 0;  // device properties, queried once per process
+    if (per_sm < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_budget_coop<1024>, 1024, 0);
+    }
     const int64_t total = (int64_t)T * G;
     int nblk = (int)std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, ceil_div(total, 4096)));
     if (per_sm < 1 || nblk < 2) {
@@ -1059,7 +1279,7 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     } else {
       int Ti = T, Gi = G, Mi = M;
       int64_t gr = groups;
-      void* args[] = {(void*)&gains, &Ti, &Gi, &gr, &Mi, &ghist, &lo_s, &hi_s, &tile_ptr};
+      void* args[] = {(void*)&gains, &Ti, &Gi, &gr, &Mi, &keybits, &ghist, &lo_s, &hi_s, &tile_ptr};
       HINM_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_budget_coop<1024>, dim3(nblk), dim3(1024),
                                                 args, 0, stream));
     }
@@ -1205,7 +1425,26 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t*
                         fast ? nullptr : p->nm_pos, fast ? nullptr : p->kept_bf16, nullptr, stream_);
     if (st) return st;
   }
-  if (fast) {
+  // fused select + operand-image pack (2:4, V in {32, 64, 128}, operand image requested)
+  const size_t kp_cap = (size_t)round_up(p->n, 64);
+  const size_t fsmem = ((kp_cap * 4 + 15) & ~size_t(15)) + 2 * (((size_t)p->n * 2 + 15) & ~size_t(15));
+  const bool fused = fast && p->a_vals && p->N == 2 && p->M == 4 &&
+                     (p->V == 32 || p->V == 64 || p->V == 128) && fsmem <= 200 * 1024 &&
+                     p->tile_kofs && p->tile_eofs && p->gidx && p->a_meta;
+  if (fused) {
+    int64_t kcap = 0, mcap = 0, acap = 0;
+    hinm_pack_capacity(p->m, p->n, p->V, p->total_keep, &kcap, &mcap, &acap);
+    if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
+    k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
+    HINM_LAUNCH_CHECK();
+    if (fsmem > 48 * 1024)
+      HINM_CUDA_TRY(cudaFuncSetAttribute(k_select_pack<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fsmem));
+    k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
+        W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
+        p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+    HINM_LAUNCH_CHECK();
+  } else if (fast) {
     constexpr int R = 4;
     if (rsmem > 48 * 1024)
       HINM_CUDA_TRY(cudaFuncSetAttribute(k_nm_select_rows<256, R>,
@@ -1221,6 +1460,6 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t*
   if (p->sigma_o != sigma_o)
     HINM_CUDA_TRY(cudaMemcpyAsync(p->sigma_o, sigma_o, (size_t)p->m * 4, cudaMemcpyDeviceToDevice,
                                   stream));
-  if (p->a_vals) return hinm_pack_build(p, stream_);
+  if (p->a_vals && !fused) return hinm_pack_build(p, stream_);
   return HINM_OK;
 }
