@@ -142,17 +142,21 @@ def run_ours(args):
     cfg = H.HiNMConfig(V, NM_N, NM_M, SV)
     g = torch.Generator(device=dev)
     packs, dense = {}, {}
-    comp_ms = {}
+    comp_ms, comp_gpu_ms = {}, {}
     for i, (name, m, n) in enumerate(layer_shapes()):
         g.manual_seed(1000 + i)                          # same weights on every rank (replicated)
         W = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
         so = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
         H.compress(W, cfg, so)                           # warm-up (allocator, cub, attributes)
         torch.cuda.synchronize()
+        ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        ce0.record()
         packs[name] = H.compress(W, cfg, so)
+        ce1.record()
         torch.cuda.synchronize()
         comp_ms[name] = (time.perf_counter() - t0) * 1e3
+        comp_gpu_ms[name] = ce0.elapsed_time(ce1)
         dense[name] = W
     g.manual_seed(7 + rank)
     X = torch.randn(N_FFN, tokens, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -160,10 +164,18 @@ def run_ours(args):
     y_up = torch.empty(M_FFN, tokens, dtype=torch.bfloat16, device=dev)
     y_down = torch.empty(N_FFN, tokens, dtype=torch.bfloat16, device=dev)
 
-    def step(x):
+    names = [nm for nm, _, _ in layer_shapes()]
+    ev = None  # per-launch CUDA events inside the timed region (roofline: per-kernel durations)
+
+    def step(x, i=None):
+        evs = ev[i] if ev is not None and i is not None else None
+        if evs: evs[0].record()
         H.spmm(packs["gate"], x, out=y_gate, order="original")
+        if evs: evs[1].record()
         H.spmm(packs["up"], x, out=y_up, order="original")
+        if evs: evs[2].record()
         H.spmm(packs["down"], y_up, out=y_down, order="original")
+        if evs: evs[3].record()
         return y_down
 
     def timed(fn, iters):
@@ -186,23 +198,21 @@ def run_ours(args):
     for _ in range(args.warmup):
         step(X)
     torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    it = iter(range(args.steps))
     with ClockSampler(local) as clk:
-        ms_total = timed(lambda: step(X), args.steps)
+        ms_total = timed(lambda: step(X, next(it)), args.steps)
+    per_kernel = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in ev) / args.steps for j, nm in enumerate(names)}
+    ev = None
     launches = 3 * args.steps                            # hinm_spmm_bf16 launches one kernel each
     assert lib.hinm_last_launch_count() == 1
     ms_step = ms_total / args.steps
     value = eff_flops(GLOBAL_TOKENS) / (ms_step * 1e-3) / 1e12
 
-    # per-kernel (roofline) and cuBLAS dense comparator on the same shapes
-    per_kernel = {}
+    # cuBLAS dense comparator on the same shapes (after our timed region)
     cublas = {}
     for name, m, n in layer_shapes():
         xin = X if name != "down" else y_up
-        out = y_down if name == "down" else y_up
-        for _ in range(3):
-            H.spmm(packs[name], xin, out=out, order="original")
-        ms_k = timed(lambda: H.spmm(packs[name], xin, out=out, order="original"), args.steps) / args.steps
-        per_kernel[name] = ms_k
         Wd = dense[name]
         for _ in range(3):
             torch.matmul(Wd, xin)
@@ -284,9 +294,14 @@ def run_ours(args):
                                  "cap_source": "scripts/l2_ring.cu on B200: 16 warps x 128-row stages, "
                                                "no MMA (profiles/r01_gather_microbench.txt)"}},
         "compressor": {"ms": {k: round(v, 3) for k, v in comp_ms.items()},
+                       "stream_ms": {k: round(v, 3) for k, v in comp_gpu_ms.items()},
                        "algorithmic_bytes": comp_bytes,
                        "gbs": round(comp_bytes / (sum(comp_ms.values()) * 1e-3) / 1e9, 1),
-                       "note": "host wall time incl. sigma validation sync, 3 layers"},
+                       "gbs_stream": round(comp_bytes / (sum(comp_gpu_ms.values()) * 1e-3) / 1e9, 1),
+                       "hbm_frac_stream": round(comp_bytes / (sum(comp_gpu_ms.values()) * 1e-3) / 1e9
+                                                / pk["hbm_gbs"], 4),
+                       "note": "ms: host wall per layer incl. allocation + sigma validation sync; "
+                               "stream_ms: CUDA events around the call; 3 layers"},
         "e2e": {"value": round(eff_flops(GLOBAL_TOKENS) / (ms_e2e * 1e-3) / 1e12, 2),
                 "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2),

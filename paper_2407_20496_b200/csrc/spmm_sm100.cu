@@ -1,25 +1,28 @@
-// HiNM SpMM on Blackwell (sm_100a): TMA gather4 of the kept activation rows + 2:4 sparse
+// HiNM SpMM on Blackwell (sm_100a): cp.async gather of the kept activation rows + 2:4 sparse
 // tcgen05.mma.sp into TMEM + fused sigma_o row-scatter epilogue.
 //
 //   Y[sigma_o[tV + r], b] = sum_k A_t[r, k] * X[gidx_t[k], b]      (spmm.py:88-98 + pruning.py:356)
 //
-// Work unit = (tile t, block of BN=256 tokens).  Persistent grid (one CTA per SM), units
+// Work unit = (tile t, block of BN = 256 tokens).  Persistent grid (one CTA per SM), units
 // distributed round-robin in token-block-major order so the X token block stays L2 resident
 // while every tile consumes it.
 //
-// Warp roles (192 threads):
-//   warp 0      producer: per 64-K stage, one bulk copy of the compressed A block (V x 64 B),
-//               one bulk copy of the 2:4 metadata every other stage (V x 16 B for 128 K), and
-//               64 TMA gather4 (16 lanes x 4 token sub-blocks) of X rows -> SWIZZLE_128B
-//               MN-major B operand (64 K-rows x 256 tokens)
-//   warp 1      TMEM allocator + single-thread MMA issuer: tcgen05.cp of the metadata into a
-//               TMEM ring, 2 x tcgen05.mma.sp (M=128, N=256, K=32) per stage, tcgen05.commit
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> bf16 -> 16 B stores to row sigma_o[tV+r]
+// Warp roles (32 * (6 + GW) threads):
+//   warps 0-3   epilogue: TMEM lane quadrant = warp; paired tcgen05.ld (16x32bx2 for M=64) ->
+//               bf16 -> 16-byte stores to row sigma_o[tV + r] (L2 evict_first)
+//   warp 4      TMEM owner + MMA issuer (one elected lane, warp-uniform loop): per X stage the
+//               metadata tcgen05.cp into a TMEM ring and 2 or 4 tcgen05.mma.sp (M = 64 for
+//               V <= 64, else 128; N = 256; K = 32)
+//   warp 5      A / metadata producer: one bulk copy per X stage (L2 evict_last) into its own
+//               deeper ring with its own barriers
+//   warps 6..   GW gather producers: 16-byte cp.async per lane, one 512-byte X row per warp
+//               instruction, SWIZZLE_128B MN-major B operand, completion via
+//               cp.async.mbarrier.arrive.noinc; indices prefetched 8 stages ahead
 //
-// V = 64 (and 32) use the M=128 instruction with rows >= V ignored: the A descriptor's upper
-// row groups alias neighbouring smem and those accumulator lanes are never read.  The M=128
-// and M=64 instructions cost the same tensor-pipe cycles (B300_MICROARCH.md: floor =
-// max(M,128)*N/256), so this costs smem read bandwidth only.
+// One accumulator: a second one (to overlap a unit's drain with the next unit's MMAs) does not
+// fit next to the metadata ring at N = 256, and N = 240 units break the 512-byte alignment of
+// the gathered row segments (gather-only time 0.72 -> 0.97 ms on the LLaMA up projection).
+// Design measurements behind this layout: profiles/r01_gather_microbench.txt.
 #include <cuda.h>
 #include <stdlib.h>
 #include <string.h>

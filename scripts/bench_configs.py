@@ -77,32 +77,37 @@ def summarize(rows, label):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of cfg1..cfg5 to run (default: all)")
     args = ap.parse_args()
+    want = lambda c: not args.only or c in args.only.split(",")
     it = 5 if args.quick else 20
     out = {"device": torch.cuda.get_device_name(), "iters": it}
     cache = {}
 
     # cfg1: BERT-base FFN 768x3072 (and the transposed reading 3072x768), 512 tokens
-    rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache), gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache)]
-    out["cfg1"] = {"rows": rows, "note": "launch/latency bound (2.4 GFLOP); the CPU reference path "
+    if want("cfg1"):
+      rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache), gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache)]
+      out["cfg1"] = {"rows": rows, "note": "launch/latency bound (2.4 GFLOP); the CPU reference path "
                    "for this config is bench.py --impl reference / cpu_baseline"}
 
     # cfg2: BERT-base, 12 layers x (Q, K, V, O 768x768; FFN1 3072x768; FFN2 768x3072), 4096 tokens
     rows = []
-    for nm, m, n, cnt in (("qkvo", 768, 768, 48), ("ffn1", 3072, 768, 12), ("ffn2", 768, 3072, 12)):
+    for nm, m, n, cnt in () if not want("cfg2") else (("qkvo", 768, 768, 48), ("ffn1", 3072, 768, 12), ("ffn2", 768, 3072, 12)):
         r = gemm_case(m, n, 4096, 64, 0.5, 11, it, cache)
         r.update({"layer": nm, "count": cnt})
         rows.append(r)
-    out["cfg2"] = {"rows": rows, "total": summarize(rows, "cfg2 BERT-base 72 GEMMs, 32x128 tokens")}
+    if rows:
+        out["cfg2"] = {"rows": rows, "total": summarize(rows, "cfg2 BERT-base 72 GEMMs, 32x128 tokens")}
 
     # cfg3: LLaMA-7B FFN, 2048..16384 tokens
     rows = []
-    for tok in (2048, 4096, 8192, 16384):
+    for tok in () if not want("cfg3") else (2048, 4096, 8192, 16384):
         for nm, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
             r = gemm_case(m, n, tok, 64, 0.5, 21, it, cache)
             r["layer"] = nm
             rows.append(r)
-    out["cfg3"] = {"rows": rows}
+    if rows:
+        out["cfg3"] = {"rows": rows}
 
     # cfg4: ResNet-50 im2col GEMMs, batch 256; conv1 (64x147) stays dense
     shapes = [(64, 64, 802816, 1), (64, 576, 802816, 3), (256, 64, 802816, 4), (64, 256, 802816, 2),
@@ -111,7 +116,7 @@ def main():
               (256, 2304, 50176, 6), (1024, 256, 50176, 6), (1024, 512, 50176, 1),
               (256, 1024, 50176, 5), (512, 1024, 50176, 1), (512, 4608, 12544, 3),
               (2048, 512, 12544, 3), (2048, 1024, 12544, 1), (512, 2048, 12544, 2)]
-    for sv, lab in ((0.5, "75%"), (0.75, "87.5%")):
+    for sv, lab in () if not want("cfg4") else ((0.5, "75%"), (0.75, "87.5%")):
         rows = []
         for m, n, tok, cnt in shapes:
             if (n * (1 - sv)) % 4:
@@ -123,10 +128,11 @@ def main():
 
     # cfg5: 4096x4096, V in {32, 64, 128} x vector-keep {50%, 25%}, 16384 tokens
     rows = []
-    for V in (32, 64, 128):
+    for V in () if not want("cfg5") else (32, 64, 128):
         for sv in (0.5, 0.75):
             rows.append(gemm_case(4096, 4096, 16384, V, sv, 41, it, cache))
-    out["cfg5"] = {"rows": rows}
+    if rows:
+        out["cfg5"] = {"rows": rows}
     print(json.dumps(out, indent=1))
 
 
