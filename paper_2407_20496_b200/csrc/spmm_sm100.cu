@@ -61,6 +61,7 @@ struct Params {
   int V;
   int units;
   int out_order;
+  int y_align32;      // Y rows 32-byte aligned: 256-bit stores
 };
 
 struct SmemLayout {
@@ -167,6 +168,14 @@ __device__ __forceinline__ void st_global_v4_hint(void* ptr, uint4 v, uint64_t p
                : "memory");
 }
 
+// 32-byte store (one full L2 sector per thread; half the LSU requests of two 16-byte stores)
+__device__ __forceinline__ void st_global_v8_hint(void* ptr, uint4 a, uint4 b, uint64_t pol) {
+  asm volatile(
+      "st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(ptr),
+      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -262,9 +271,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32
 // with the number of warps issuing cp.async, not with the bytes in flight (scripts/l2_cap.cu on
 // B200: 8 warps/SM 15.6 TB/s, 12 -> 19.2, 16 -> 21.0 TB/s at any depth), so the default runs
 // 16 gather warps.
-constexpr int MMA_WARP = 4;
-constexpr int AE_WARP = 5;
-constexpr int GATHER_WARP0 = 6;
+constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant (column halves)
+constexpr int MMA_WARP = 8;
+constexpr int AE_WARP = 9;
+constexpr int GATHER_WARP0 = 10;
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -322,9 +332,9 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
   const uint32_t bar_acc_empty = bar_acc_full + 8;
   const int AST = (int)L.ast;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
-  // TMEM lane quadrants (= epilogue warps) that hold real rows
+  // TMEM lane quadrants that hold real rows; two epilogue warps (column halves) per quadrant
   const int n_quads = M64 ? V / 16 : (V >= 128 ? 4 : V / 32);
-  const int n_epi_warps = n_quads;
+  const int n_epi_warps = 2 * n_quads;
 
   // constant metadata for lanes the producer never writes (rows >= V, M=64 gap lanes)
   if (M64) {
@@ -542,20 +552,22 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       __syncwarp();
     }
   } else {
-    // ============================================================ epilogue (warps 0-3)
-    // The accumulator is drained with 32-column tcgen05.ld's and released to the MMA issuer right
-    // after the LAST load, before that chunk's bf16 conversion and stores.
-    //   M=64 : row 16q + (lane & 15); chunk c = columns 32c + 128(lane >= 16) + [0, 32), c < 4
-    //          (16x32bx2: lanes 0-15 of the quadrant hold the 16 accumulator rows, so all 32
-    //          threads of the warp carry data)
-    //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c < 8   (32x32b)
-    const int q = warp;
+    // ============================================================ epilogue (warps 0-7)
+    // Warp w drains TMEM lane quadrant q = w & 3, column half h = w >> 2, with 32-column
+    // tcgen05.ld's issued in pairs, and releases the accumulator to the MMA issuer right after
+    // its last load, before that chunk's bf16 conversion and stores.  The drain is the
+    // critical path between consecutive units (the next unit's MMAs wait for it): with small K
+    // it dominated the kernel (scripts/spmm_shape.py, HINM_GATHER=dbg_noepi), hence 8 warps.
+    //   M=64 : row 16q + (lane & 15); chunk c = columns 32c + 128(lane >= 16) + [0, 32),
+    //          c in {2h, 2h + 1}  (16x32bx2: lanes 0-15 of the quadrant hold the 16 rows)
+    //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c in [4h, 4h + 4)
+    const int q = warp & 3, h = warp >> 2;
     if (q < n_quads) {
       uint32_t ucount = 0;
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
       const int c_own = M64 && lane >= 16 ? 128 : 0;
-      constexpr int NCH = M64 ? 4 : 8;
-      const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16);
+      constexpr int NCH = M64 ? 2 : 4;  // chunks per warp
+      const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16) + h * NCH * 32;
       auto out_row = [&](const UnitParams& u) -> int64_t {
         const int64_t prow = (int64_t)u.t * V + r;
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
@@ -563,6 +575,22 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       // 32 accumulator columns (fp32 bits) -> bf16 -> 4 x 16-byte stores of one row segment
       const uint64_t pol_y = l2_policy_evict_first();
       auto store32 = [&](uint16_t* yrow, int col, const uint32_t (&v)[32]) {
+        if (p.y_align32 && col + 32 <= p.B) {  // 2 x 32-byte stores: one full sector each
+#pragma unroll
+          for (int j = 0; j < 4; j += 2) {
+            uint4 a, b;
+            a.x = pack_bf16x2(v[j * 8 + 0], v[j * 8 + 1]);
+            a.y = pack_bf16x2(v[j * 8 + 2], v[j * 8 + 3]);
+            a.z = pack_bf16x2(v[j * 8 + 4], v[j * 8 + 5]);
+            a.w = pack_bf16x2(v[j * 8 + 6], v[j * 8 + 7]);
+            b.x = pack_bf16x2(v[j * 8 + 8], v[j * 8 + 9]);
+            b.y = pack_bf16x2(v[j * 8 + 10], v[j * 8 + 11]);
+            b.z = pack_bf16x2(v[j * 8 + 12], v[j * 8 + 13]);
+            b.w = pack_bf16x2(v[j * 8 + 14], v[j * 8 + 15]);
+            st_global_v8_hint(yrow + col + j * 8, a, b, pol_y);
+          }
+          return;
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (col + j * 8 < p.B) {
@@ -583,7 +611,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         nxt = unit_params(p, u + gridDim.x);
         if (u + (int)gridDim.x < p.units) nxt_row = out_row(nxt);
         uint16_t* yrow = p.Y + orow * p.ldy;
-        const int col_base = cur.nb * BN + c_own;
+        const int col_base = cur.nb * BN + c_own + h * NCH * 32;
         if (cur.kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
           for (int c = 0; c < NCH * 4; ++c)
             if (col_base + c * 8 < p.B)
@@ -593,6 +621,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         mbar_wait(bar_acc_full, ucount & 1);
         ++ucount;
         tc_fence_after();
+        if (DBG == 3) {  // experiment: release at once, no drain / stores
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_acc_empty);
+          continue;
+        }
         // chunks are loaded in pairs (two tcgen05.ld in flight, one wait); the accumulator is
         // released after the last pair's wait
         uint32_t v0[32], v1[32];
@@ -671,12 +704,14 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int nbk = (B + BN - 1) / BN;
   prm.units = nbk * pk->T;
   prm.out_order = out_order;
+  static const int env_v8 = getenv("HINM_Y_V8") ? atoi(getenv("HINM_Y_V8")) : 1;
+  prm.y_align32 = env_v8 && (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
   const int grid = std::min(prm.units, sm_count());
   // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 contend
   // with the MMA for shared-memory bandwidth); V <= 64 -> 128-row X stages; V = 128 -> 64-row
   // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
   // Experiments: HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128 (M=128 instruction for
-  // V <= 64) | dbg_nomma | dbg_nogather (timing only: the results are garbage).
+  // V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi (timing only: the results are garbage).
   static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
   static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
   static const int variant = [] {
@@ -685,6 +720,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "m128")) return 1;
     if (!strcmp(e, "dbg_nomma")) return 2;
     if (!strcmp(e, "dbg_nogather")) return 3;
+    if (!strcmp(e, "dbg_noepi")) return 4;
     return 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
@@ -702,6 +738,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 1, true>, 128, 8);
   } else if (variant == 3) {
     rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8);
+  } else if (variant == 4) {
+    rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8);
   } else if (ks == 128) {
     rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true>, 128, 8) : launch(k_hinm_spmm<128, 8, 0, false>, 128, 8))
                  : (m64 ? launch(k_hinm_spmm<128, 16, 0, true>, 128, 16) : launch(k_hinm_spmm<128, 16, 0, false>, 128, 16));
