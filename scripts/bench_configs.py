@@ -39,6 +39,8 @@ def timed(fn, iters):
 
 
 def gemm_case(m, n, tokens, V, sv, seed, iters, cublas_cache=None):
+    if os.environ.get("EMPTY_CACHE"):
+        torch.cuda.empty_cache()
     g = torch.Generator(device=DEV).manual_seed(seed)
     W = torch.randn(m, n, generator=g, device=DEV).to(torch.bfloat16)
     X = torch.randn(n, tokens, generator=g, device=DEV).to(torch.bfloat16)
@@ -84,6 +86,16 @@ def main():
     out = {"device": torch.cuda.get_device_name(), "iters": it}
     cache = {}
 
+    # cfg3: LLaMA-7B FFN, 2048..16384 tokens
+    rows = []
+    for tok in () if not want("cfg3") else (2048, 4096, 8192, 16384):
+        for nm, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
+            r = gemm_case(m, n, tok, 64, 0.5, 21, it, cache)
+            r["layer"] = nm
+            rows.append(r)
+    if rows:
+        out["cfg3"] = {"rows": rows}
+
     # cfg1: BERT-base FFN 768x3072 (and the transposed reading 3072x768), 512 tokens
     if want("cfg1"):
       rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache), gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache)]
@@ -98,16 +110,6 @@ def main():
         rows.append(r)
     if rows:
         out["cfg2"] = {"rows": rows, "total": summarize(rows, "cfg2 BERT-base 72 GEMMs, 32x128 tokens")}
-
-    # cfg3: LLaMA-7B FFN, 2048..16384 tokens
-    rows = []
-    for tok in () if not want("cfg3") else (2048, 4096, 8192, 16384):
-        for nm, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
-            r = gemm_case(m, n, tok, 64, 0.5, 21, it, cache)
-            r["layer"] = nm
-            rows.append(r)
-    if rows:
-        out["cfg3"] = {"rows": rows}
 
     # cfg4: ResNet-50 im2col GEMMs, batch 256; conv1 (64x147) stays dense
     shapes = [(64, 64, 802816, 1), (64, 576, 802816, 3), (256, 64, 802816, 4), (64, 256, 802816, 2),
