@@ -15,8 +15,11 @@ from .model import (DenseMatrix, GyroPermutation, HiNMConfig, MaskPair, Saliency
 from .pruning import (HiNMEncoding, TileEncoding, apply_masks, decode, encode, encoding_from_pack,
                       load_saliency, magnitude_saliency, masked_dense_from_encoding, nm_prune,
                       restore_row_order, survivors_per_tile, validate_masks, vector_prune)
-from .spmm import (TileBuffer, dense_matmul, gather_tile_buffer, hinm_spmm,
-                   hinm_spmm_original_order, relative_error)
+from .spmm import (LayerChain, TileBuffer, build_layer_chain, compose_layers, dense_matmul,
+                   gather_tile_buffer, hinm_spmm, hinm_spmm_original_order, kept_triples,
+                   relative_error, shuffle_encoding, tile_shuffle_check)
+from .spmm import _identity_permute as no_perm_prune
+from . import io
 from .device import DevicePack, HostChain, build_operand_image, compress, spmm, spmm_simt
 
 __version__ = "0.1.0"
@@ -31,5 +34,7 @@ __all__ = [
     "masked_dense_from_encoding", "nm_prune", "restore_row_order", "survivors_per_tile",
     "validate_masks", "vector_prune", "TileBuffer", "dense_matmul", "gather_tile_buffer",
     "hinm_spmm", "hinm_spmm_original_order", "relative_error", "DevicePack",
-    "build_operand_image", "compress", "spmm", "spmm_simt", "HostChain",
+    "build_operand_image", "compress", "spmm", "spmm_simt", "HostChain", "LayerChain",
+    "build_layer_chain", "compose_layers", "kept_triples", "shuffle_encoding",
+    "tile_shuffle_check", "no_perm_prune", "io",
 ]

@@ -97,5 +97,192 @@ def relative_error(result, reference) -> float:
     return float(np.abs(r - ref).max(initial=0.0)) / scale
 
 
+# --------------------------------------------------------------------------------------------
+# Group-order freedom and its validation (spmm.py:113-203)
+
+def kept_triples(enc: HiNMEncoding) -> set:
+    """{(original row, original column, value)} kept by an encoding (spmm.py:113-130)."""
+    cfg = enc.config
+    V, N, M = cfg.vector_size, cfg.nm_keep, cfg.nm_group
+    so = np.asarray(enc.sigma_o, dtype=np.int64)
+    out = set()
+    for t, tile in enumerate(enc.tiles):
+        k = np.asarray(tile.vector_index).size
+        if k == 0:
+            continue
+        G = k // M
+        groups = np.asarray(tile.vector_index, dtype=np.int64).reshape(G, M)
+        pos = np.asarray(tile.nm_index, dtype=np.int64).reshape(V, G, N)
+        vals = np.asarray(tile.kept_values, dtype=np.float64).reshape(V, G, N)
+        cols = groups[np.arange(G)[None, :, None], pos]                # (V, G, N)
+        rows = np.broadcast_to(so[t * V:(t + 1) * V, None, None], cols.shape)
+        out.update(zip(rows.ravel().tolist(), cols.ravel().tolist(), vals.ravel().tolist()))
+    return out
+
+
+def shuffle_encoding(enc: HiNMEncoding, rng) -> HiNMEncoding:
+    """Reorder each tile's vector index at group granularity (and within groups), rewriting
+    nm_index / kept_values so the kept set is unchanged (spmm.py:133-180).  Draws from `rng`
+    in the reference's order (one permutation of the groups, then one of M per group), so the
+    same generator state yields the reference's shuffle."""
+    cfg = enc.config
+    V, N, M = cfg.vector_size, cfg.nm_keep, cfg.nm_group
+    tiles = []
+    for tile in enc.tiles:
+        k = np.asarray(tile.vector_index).size
+        if k == 0:
+            tiles.append(tile)
+            continue
+        G = k // M
+        group_order = rng.permutation(G)
+        within = np.stack([rng.permutation(M) for _ in range(G)])      # (G, M): new slot -> old slot
+        old_groups = np.asarray(tile.vector_index, dtype=np.int64).reshape(G, M)
+        new_index = old_groups[group_order[:, None], within].reshape(-1)
+        inverse = np.argsort(within, axis=1)                            # (G, M): old slot -> new slot
+        old_pos = np.asarray(tile.nm_index, dtype=np.int64).reshape(V, G, N)[:, group_order, :]
+        old_vals = np.asarray(tile.kept_values, dtype=np.float64).reshape(V, G, N)[:, group_order, :]
+        moved = inverse[np.arange(G)[None, :, None], old_pos]           # (V, G, N) new positions
+        order = np.argsort(moved, axis=2, kind="stable")
+        tiles.append(TileEncoding(vector_index=new_index,
+                                  nm_index=np.take_along_axis(moved, order, 2).reshape(V, -1),
+                                  kept_values=np.take_along_axis(old_vals, order, 2).reshape(V, -1)))
+    return HiNMEncoding(shape=enc.shape, config=enc.config, sigma_o=enc.sigma_o, tiles=tiles)
+
+
+def _product_f32(enc: HiNMEncoding, X):
+    """fp32-output product of an encoding on the GPU (CUDA-core kernel; validation use)."""
+    torch = _torch()
+    pack = pack_from_encoding_nocache(enc, X.device)
+    return _spmm_simt(pack, X, order="sigma").double()
+
+
+def pack_from_encoding_nocache(enc, device):
+    from .pruning import pack_from_encoding
+
+    return pack_from_encoding(enc, device)
+
+
+def tile_shuffle_check(enc: HiNMEncoding, inputs, rng, trials: int = 50,
+                       tolerance: float = 1e-5) -> dict:
+    """Within-tile vector order does not change the product (spmm.py:183-203).
+
+    Each trial reshuffles every tile (same rng stream as the reference), compares the kept
+    (row, column, value) sets, and measures the product difference.  Products run on the GPU
+    with fp32 outputs (the CUDA-core kernel over the reference view: only the fp32 summation
+    order changes, well inside the reference's 1e-5); ``tc_max_relative_error`` additionally
+    reports the tcgen05 path, whose bf16 output rounding can move by one bf16 ulp.
+    """
+    torch = _torch()
+    Xh = as_values(inputs)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X = torch.as_tensor(Xh.astype(np.float32)).to(dev).to(torch.bfloat16)
+    base = _product_f32(enc, X)
+    base_tc = None
+    base_triples = kept_triples(enc)
+    tc_ok = spmm_supported(enc.config.vector_size, enc.config.nm_keep, enc.config.nm_group)
+    if tc_ok:
+        base_tc = torch.as_tensor(hinm_spmm(pack_from_encoding_nocache(enc, dev), X)).double()
+    errors, tc_errors, kept_equal = [], [], True
+    for _ in range(trials):
+        sh = shuffle_encoding(enc, rng)
+        kept_equal = kept_equal and (kept_triples(sh) == base_triples)
+        errors.append(relative_error(_product_f32(sh, X).cpu().numpy(), base.cpu().numpy()))
+        if tc_ok:
+            y = torch.as_tensor(hinm_spmm(pack_from_encoding_nocache(sh, dev), X)).double()
+            tc_errors.append(relative_error(y.cpu().numpy(), base_tc.cpu().numpy()))
+    max_err = max(errors) if errors else 0.0
+    return {"trials": trials, "kept_sets_equal": bool(kept_equal), "max_relative_error": max_err,
+            "errors": errors, "tolerance": tolerance,
+            "passed": bool(kept_equal and max_err <= tolerance),
+            "tc_max_relative_error": max(tc_errors) if tc_errors else None}
+
+
+# --------------------------------------------------------------------------------------------
+# Multi-layer chains without restore (spmm.py:206-244; SURVEY §8(f) row 3)
+
+@dataclass(frozen=True)
+class LayerChain:
+    """Encoded layers; layer l consumes layer l-1's output rows in their sigma_o order."""
+
+    layers: tuple
+
+
+def _identity_permute(W, cfg, saliency=None):
+    """The reference's ``no_perm_prune`` (permutation.py:644-646): identity sigma_o, ascending
+    survivors as sigma_i -- the GPU compressor's own-sigma_i mode."""
+    from .model import GyroPermutation, MaskPair, ensure_validated
+    from .pruning import magnitude_saliency, nm_prune, survivors_per_tile, vector_prune
+
+    m, n = as_values(W).shape
+    vcfg = ensure_validated(cfg, (m, n))
+    S = magnitude_saliency(W) if saliency is None else saliency
+    so = np.arange(m, dtype=np.int64)
+    vm = vector_prune(S, vcfg.config, so)
+    sigma = GyroPermutation(sigma_o=so, sigma_i=tuple(survivors_per_tile(vm)))
+    return sigma, MaskPair(vector_mask=np.asarray(vm), element_mask=np.asarray(
+        nm_prune(S, vm, vcfg.config, sigma))), None
+
+
+def build_layer_chain(weight_matrices, cfgs, saliencies=None, permute=None) -> LayerChain:
+    """Prune and encode a stack of layers with offline pre-permutation (spmm.py:206-234):
+    layer l's columns are reordered by layer l-1's sigma_o before pruning, so at run time each
+    layer consumes its predecessor's output rows directly (no restore between layers).
+
+    ``permute(W, cfg, saliency=...) -> (GyroPermutation, MaskPair, report)`` is the permutation
+    search; the reference uses ``gyro_permute`` (permutation.py:549), which is outside this GPU
+    path -- pass it in to reproduce the reference exactly.  The default is the
+    identity pipeline (``no_perm_prune``).
+    """
+    from .pruning import encode
+
+    permute = permute or _identity_permute
+    if not isinstance(cfgs, (list, tuple)):
+        cfgs = [cfgs] * len(weight_matrices)
+    if saliencies is None:
+        saliencies = [None] * len(weight_matrices)
+    layers, prev = [], None
+    for W, cfg, sal in zip(weight_matrices, cfgs, saliencies):
+        Wv = as_values(W)
+        Sv = None if sal is None else as_values(sal)
+        if prev is not None:
+            if Wv.shape[1] != prev.size:
+                raise ShapeMismatch(f"layer expects {Wv.shape[1]} inputs, previous layer emits {prev.size}")
+            Wv = Wv[:, prev]
+            Sv = None if Sv is None else Sv[:, prev]
+        sigma, masks, _ = permute(Wv, cfg, saliency=Sv)
+        layers.append(encode(Wv, masks, sigma, cfg))
+        prev = np.asarray(sigma.sigma_o, dtype=np.int64)
+    return LayerChain(layers=tuple(layers))
+
+
+def compose_layers(chain: LayerChain, inputs):
+    """Run a chain end to end (spmm.py:237-244): every layer on the GPU with the activations
+    kept resident between layers (bf16, fp32 accumulation); rows of the result are in the last
+    layer's sigma_o order.  Host inputs return float64 numpy, CUDA inputs a CUDA tensor."""
+    torch = _torch()
+    on_dev = _is_cuda(inputs)
+    if on_dev:
+        X = inputs
+    else:
+        Xh = as_values(inputs)
+        X = torch.as_tensor(Xh.astype(np.float32)).to(torch.device("cuda", torch.cuda.current_device()))
+    B = X.shape[1]
+    Bp = max(8, -(-B // 8) * 8)
+    Xb = torch.zeros(X.shape[0], Bp, dtype=torch.bfloat16, device=X.device)
+    Xb[:, :B] = X.to(torch.bfloat16)
+    for enc in chain.layers:
+        pack = enc if isinstance(enc, DevicePack) else enc.device_pack(X.device)
+        if Xb.shape[0] != pack.n:
+            raise ShapeMismatch(f"input has {Xb.shape[0]} rows, encoding expects {pack.n}")
+        if spmm_supported(pack.V, pack.N, pack.M):
+            Xb = _spmm_tc(pack, Xb, order="sigma")
+        else:
+            Xb = _spmm_simt(pack, Xb, order="sigma").to(torch.bfloat16)
+    Y = Xb[:, :B]
+    return Y if on_dev else Y.float().cpu().numpy().astype(np.float64)
+
+
 __all__ = ["TileBuffer", "gather_tile_buffer", "hinm_spmm", "hinm_spmm_original_order",
-           "dense_matmul", "relative_error", "restore_row_order", "HiNMEncoding"]
+           "dense_matmul", "relative_error", "restore_row_order", "HiNMEncoding",
+           "kept_triples", "shuffle_encoding", "tile_shuffle_check", "LayerChain",
+           "build_layer_chain", "compose_layers"]

@@ -70,7 +70,8 @@ def test_status_codes_map_to_reference_exceptions():
 
 
 def test_sass_has_tcgen05_and_tma():
-    """The SpMM kernel is compiled to tcgen05 MMA (UTCHMMA), TMEM (LDTM/UTCCP) and TMA gather4."""
+    """The SpMM kernel is compiled to tcgen05 MMA (UTCHMMA), TMEM (LDTM / UTCCP), bulk copies
+    (UBLKCP, the A / metadata image), cp.async gather (LDGSTS) and 256-bit Y stores."""
     import shutil
     import subprocess
 
@@ -80,5 +81,5 @@ def test_sass_has_tcgen05_and_tma():
 
         pytest.skip("cuobjdump not available")
     sass = subprocess.run([cuobjdump, "-sass", _lib_path()], capture_output=True, text=True).stdout
-    for mnem in ("UTCHMMA", "UTCCP", "LDTM", "UTMALDG.2D.GATHER4", "UBLKCP"):
+    for mnem in ("UTCHMMA", "UTCCP", "LDTM", "UBLKCP", "LDGSTS", "STG.E.ENL2.256"):
         assert mnem in sass, mnem
