@@ -81,5 +81,5 @@ def test_sass_has_tcgen05_and_tma():
 
         pytest.skip("cuobjdump not available")
     sass = subprocess.run([cuobjdump, "-sass", _lib_path()], capture_output=True, text=True).stdout
-    for mnem in ("UTCHMMA", "UTCCP", "LDTM", "UBLKCP", "LDGSTS", "STG.E.ENL2.256"):
+    for mnem in ("UTCHMMA", "UTCCP", "LDTM", "UBLKCP", "LDGSTS", "ENL2.256"):
         assert mnem in sass, mnem
