@@ -187,6 +187,22 @@ int hinm_spmm_simt_f32(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, 
 /* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
 int hinm_last_launch_count(void);
 
+/*
+ * Gyro-permutation search kernels (the search driver is
+ * paper_2407_20496_b200/permutation.py).
+ *
+ * hinm_icp_costs  <- the ICP cost double loop of icp_tile                  permutation.py:414-421
+ *   vals: DEVICE V x k fp64 (row-major, one tile's surviving columns), rem: G x (M-1) and
+ *   samp: G column ids into vals (DEVICE int32), costs: DEVICE G x G fp64.  Bit-identical to
+ *   the reference (numpy pairwise sums in memory order).  Async.
+ * hinm_lex_assignment <- hungarian (lexicographically smallest optimal matching) permutation.py:199-235
+ *   C: HOST n x n fp64, assignment: HOST int64[n].  O(n^3) host code (the reference's O(n^2)
+ *   linear_sum_assignment calls become one matching + one Dijkstra per row).  Synchronous.
+ */
+int hinm_icp_costs(const double* vals, int V, int k, const int32_t* rem, const int32_t* samp,
+                   int G, int M, int N, double* costs, void* stream);
+int hinm_lex_assignment(const double* C, int n, int64_t* assignment);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,9 @@ from .pruning import (HiNMEncoding, TileEncoding, apply_masks, decode, encode, e
 from .spmm import (LayerChain, TileBuffer, build_layer_chain, compose_layers, dense_matmul,
                    gather_tile_buffer, hinm_spmm, hinm_spmm_original_order, kept_triples,
                    relative_error, shuffle_encoding, tile_shuffle_check)
-from .spmm import _identity_permute as no_perm_prune
+from .permutation import (PruneReport, ablation_mode, balanced_kmeans, gyro_permute, hungarian,
+                          icp_tile, no_perm_prune, ocp_iterate, retained_saliency,
+                          sample_channels)
 from . import io
 from .device import DevicePack, HostChain, build_operand_image, compress, spmm, spmm_simt
 
@@ -36,5 +38,7 @@ __all__ = [
     "hinm_spmm", "hinm_spmm_original_order", "relative_error", "DevicePack",
     "build_operand_image", "compress", "spmm", "spmm_simt", "HostChain", "LayerChain",
     "build_layer_chain", "compose_layers", "kept_triples", "shuffle_encoding",
-    "tile_shuffle_check", "no_perm_prune", "io",
+    "tile_shuffle_check", "no_perm_prune", "io", "PruneReport", "ablation_mode",
+    "balanced_kmeans", "gyro_permute", "hungarian", "icp_tile", "ocp_iterate",
+    "retained_saliency", "sample_channels",
 ]

@@ -1,0 +1,76 @@
+"""GPU: the gyro-permutation search (§8(f) row 1) against the reference's own runs
+(tests/golden/gyro.npz + gyro_reports.json, generator tests/golden/make_golden_gyro.py):
+identical sigma_o, sigma_i, both masks and the whole PruneReport (every retention log entry
+bit-equal) for OCP + ICP runs, the ablation variants and a tie-heavy matrix; plus the ICP cost
+kernel against the reference's double loop."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2407_20496_b200 as H  # noqa: E402
+from paper_2407_20496_b200 import permutation as P  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+with open(os.path.join(GOLD, "gyro_reports.json")) as fh:
+    REPORTS = json.load(fh)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.fixture(scope="module")
+def g():
+    return np.load(os.path.join(GOLD, "gyro.npz"))
+
+
+@pytest.mark.parametrize("name", sorted(REPORTS))
+def test_gyro_permute_matches_reference(g, name):
+    m, n, V, N, M, sv, oi, ii, seed, ocs, ics = REPORTS[name]["cfg"]
+    cfg = H.HiNMConfig(vector_size=V, nm_keep=N, nm_group=M, vector_sparsity=sv,
+                       ocp_max_iters=oi, icp_max_iters=ii, seed=seed)
+    sigma, masks, rep = P.gyro_permute(g[f"{name}_W"], cfg, ocp_strategy=ocs, icp_strategy=ics)
+    assert np.array_equal(sigma.sigma_o, g[f"{name}_sigma_o"])
+    lens = g[f"{name}_sigma_i_len"]
+    assert [len(o) for o in sigma.sigma_i] == lens.tolist()
+    assert np.array_equal(np.concatenate(sigma.sigma_i), g[f"{name}_sigma_i"])
+    assert np.array_equal(masks.vector_mask, g[f"{name}_vmask"])
+    assert np.array_equal(masks.element_mask, g[f"{name}_emask"])
+    assert rep.to_dict() == REPORTS[name]["report"]
+
+
+def _ref_icp_costs(vals, rem, samp, N):
+    G = len(samp)
+    C = np.empty((G, G))
+    for i in range(G):
+        base = vals[:, rem[i]]
+        bt = float(base.sum())
+        for j in range(G):
+            union = np.concatenate([base, vals[:, [samp[j]]]], axis=1)
+            kept = float(np.sort(union, axis=1)[:, -N:].sum())
+            C[i, j] = bt + float(vals[:, samp[j]].sum()) - kept
+    return C
+
+
+@pytest.mark.parametrize("V,M,N", [(64, 4, 2), (128, 4, 2), (16, 4, 1), (8, 8, 3)])
+def test_icp_cost_kernel_bit_exact(V, M, N):
+    rng = np.random.default_rng(V + M + N)
+    tile = np.abs(rng.standard_normal((V, 96))) * rng.choice([1.0, 1e-3, 1e2], size=(V, 96))
+    surv = np.sort(rng.permutation(96)[:M * 10])
+    vals = tile[:, surv]
+    G = 10
+    groups = [list(range(q * M, (q + 1) * M)) for q in range(G)]
+    picks = [int(rng.integers(M)) for _ in groups]
+    samp = [grp[p] for grp, p in zip(groups, picks)]
+    rem = [[x for q, x in enumerate(grp) if q != p] for grp, p in zip(groups, picks)]
+    ref = _ref_icp_costs(vals, rem, samp, N)
+    got = P._IcpCostsGPU(vals, M, N)(np.array(rem), np.array(samp))
+    assert np.array_equal(got, ref)
