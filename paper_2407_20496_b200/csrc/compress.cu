@@ -296,7 +296,7 @@ struct AndOp {
 };
 
 template <int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_tile_sort(const double* __restrict__ scores, int n,
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const double* __restrict__ scores, int n,
                                                   double* __restrict__ sorted,
                                                   int32_t* __restrict__ order) {
   typedef cub::BlockRadixSort<uint64_t, NT, ITEMS, int32_t, 6> BRS;
@@ -1152,21 +1152,32 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   return HINM_OK;
 }
 
-template <int ITEMS>
+template <int ITEMS, int NT = 1024>
 int launch_tile_sort_items(const double* scores, int n, int T, double* sorted, int32_t* order,
                            cudaStream_t stream) {
-  typedef cub::BlockRadixSort<uint64_t, 1024, ITEMS, int32_t, 6> BRS;
+  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS, int32_t, 6> BRS;
   const size_t smem = sizeof(typename BRS::TempStorage);
   if (smem > 48 * 1024)
-    HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<1024, ITEMS>,
+    HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<NT, ITEMS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_tile_sort<1024, ITEMS><<<T, 1024, smem, stream>>>(scores, n, sorted, order);
+  k_tile_sort<NT, ITEMS><<<T, NT, smem, stream>>>(scores, n, sorted, order);
   HINM_LAUNCH_CHECK();
   return HINM_OK;
 }
 
 int launch_tile_sort(const double* scores, int n, int T, double* sorted, int32_t* order,
                      cudaStream_t stream) {
+  // more tiles than SMs: 512-thread CTAs, two per SM, so every tile sorts in the first wave
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (T > sms && n > 1024 && n <= 4096) {
+    if (n <= 2048) return launch_tile_sort_items<4, 512>(scores, n, T, sorted, order, stream);
+    return launch_tile_sort_items<8, 512>(scores, n, T, sorted, order, stream);
+  }
   if (n <= 1024) return launch_tile_sort_items<1>(scores, n, T, sorted, order, stream);
   if (n <= 2048) return launch_tile_sort_items<2>(scores, n, T, sorted, order, stream);
   if (n <= 4096) return launch_tile_sort_items<4>(scores, n, T, sorted, order, stream);
