@@ -288,6 +288,10 @@ def run_ours(args):
                      "peak_source": f"2 x bf16_tflops of {kind} MEASURED_PEAKS.json (2:4 sparse)",
                      "algorithmic": "2*m*k_bar*tokens per SpMM (k_bar = n/2 kept vectors)",
                      "traffic_note": (tr or {}).get("note"),
+                     # the V=64 tile runs on the M=64 sparse instruction: 144 cycles per
+                     # 64x256x32 MMA = 1964 TF/s logical on 148 SMs (scripts/mma_rate.cu)
+                     "instruction_ceiling": 1964.4,
+                     "frac_of_instruction_ceiling": round(achieved / 1964.4, 4),
                      "binding": {"resource": "L2->SMEM gather (cp.async)",
                                  "achieved_tbs": round(l2_tbs, 2), "cap_tbs": 21.2,
                                  "frac": round(l2_tbs / 21.2, 3),

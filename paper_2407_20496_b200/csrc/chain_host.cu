@@ -9,6 +9,7 @@
 // their sum.  Three chunk slots of device scratch live in the caller's workspace.
 #include <algorithm>
 #include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -91,11 +92,39 @@ extern "C" int hinm_chain_run_host(const hinm_chain_step_t* steps, int nsteps, c
   HINM_CUDA_TRY(cudaEventRecord(cs->comp_done[0], st));
   HINM_CUDA_TRY(cudaStreamWaitEvent(cs->h2d, cs->comp_done[0], 0));
   HINM_CUDA_TRY(cudaStreamWaitEvent(cs->d2h, cs->comp_done[0], 0));
-  const int nchunks = (B + chunk_tokens - 1) / chunk_tokens;
+  // Chunk schedule: the pipeline fills with a quarter chunk and drains with a quarter chunk
+  // (the first H2D and the last D2H are not overlapped with anything), full chunks in between.
+  std::vector<int> starts, widths;
+  {
+    const int ramp = std::max(8, (chunk_tokens / 4) / 8 * 8);
+    int c0 = 0;
+    if (B > 2 * chunk_tokens) {
+      starts.push_back(0);
+      widths.push_back(ramp);
+      c0 = ramp;
+    }
+    while (c0 < B) {
+      int w = std::min(chunk_tokens, B - c0);
+      const int left = B - c0 - w;
+      if (left > 0 && left < ramp) w = B - c0 - ramp;  // keep a quarter chunk for the drain
+      starts.push_back(c0);
+      widths.push_back(w);
+      c0 += w;
+    }
+    // split the final full chunk so the drain is a quarter chunk
+    if (widths.size() >= 3 && widths.back() > ramp) {
+      const int wl = widths.back();
+      const int s0 = starts.back();
+      widths.back() = wl - ramp;
+      starts.push_back(s0 + wl - ramp);
+      widths.push_back(ramp);
+    }
+  }
+  const int nchunks = (int)starts.size();
   for (int c = 0; c < nchunks; ++c) {
     const int slot = c % NSLOT;
-    const int c0 = c * chunk_tokens;
-    const int w = std::min(chunk_tokens, B - c0);
+    const int c0 = starts[c];
+    const int w = widths[c];
     // H2D of the chain input once the slot's previous compute has consumed it
     if (c >= NSLOT) HINM_CUDA_TRY(cudaStreamWaitEvent(cs->h2d, cs->comp_done[slot], 0));
     HINM_CUDA_TRY(cudaMemcpy2DAsync(buf(slot, 0), (size_t)chunk_tokens * 2, X_host + c0, (size_t)ldx * 2,
