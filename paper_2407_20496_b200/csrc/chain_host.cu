@@ -7,6 +7,8 @@
 // i-2's device->host copy run concurrently on three streams (two internal copy streams plus the
 // caller's compute stream), so the end-to-end time approaches max(H2D, compute, D2H) instead of
 // their sum.  Three chunk slots of device scratch live in the caller's workspace.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <unordered_map>
 #include <vector>
@@ -133,7 +135,8 @@ extern "C" int hinm_chain_run_host(const hinm_chain_step_t* steps, int nsteps, c
     // compute: after the input arrived and the slot's previous result was copied out
     HINM_CUDA_TRY(cudaStreamWaitEvent(st, cs->h2d_done[slot], 0));
     if (c >= NSLOT) HINM_CUDA_TRY(cudaStreamWaitEvent(st, cs->d2h_done[slot], 0));
-    for (int i = 0; i < nsteps; ++i) {
+    static const bool no_compute = getenv("HINM_CHAIN_NOCOMPUTE") != nullptr;  // diagnostics
+    for (int i = 0; i < nsteps && !no_compute; ++i) {
       const hinm_chain_step_t& s = steps[i];
       rc = hinm_spmm_bf16(s.pack, buf(slot, s.src), chunk_tokens, w, buf(slot, s.dst), chunk_tokens,
                           s.out_order, st);

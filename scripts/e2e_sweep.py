@@ -36,7 +36,7 @@ def duplex():
     torch.cuda.current_stream().wait_stream(s1)
     torch.cuda.current_stream().wait_stream(s2)
 out["duplex_each_gbs"] = round(xh.numel() * 2 / t(duplex) / 1e6, 1)
-for chunk in (2048,):
+for chunk in (1024, 2048, 4096):
     ch = H.HostChain([(packs["gate"], 0, 1, "original"), (packs["up"], 0, 2, "original"),
                       (packs["down"], 2, 3, "original")], out_buf=3, chunk=chunk, device=dev)
     out[f"e2e_ms_chunk{chunk}"] = round(t(lambda: ch.run(xh, yh)), 4)
