@@ -136,7 +136,13 @@ extern "C" int hinm_lex_assignment(const double* C, int n, int64_t* assignment) 
   for (int64_t i = 0; i < (int64_t)n * n; ++i) absC[i] = fabs(C[i]);
   const double tol = 1e-9 * std::max(1.0, np_pairwise(absC.data(), (int64_t)n * n));
 
+  // C transposed: the per-row Dijkstra reads column bmin of C for every unfixed row
+  std::vector<double> CT((size_t)n * n);
+  for (int r = 0; r < n; ++r)
+    for (int b = 0; b < n; ++b) CT[(size_t)b * n + r] = C[(size_t)r * n + b];
   std::vector<char> col_alive(n, 1);
+  std::vector<int> alive(n), open;
+  for (int b = 0; b < n; ++b) alive[b] = b;
   std::vector<double> dist(n);
   std::vector<int> next(n), done(n);
   double prefix = 0.0;
@@ -148,27 +154,35 @@ extern "C" int hinm_lex_assignment(const double* C, int n, int64_t* assignment) 
     const int ci = col_of[i];
     // reverse Dijkstra from ci: dist[b] = cheapest way to free ci starting by vacating b
     // (row_of[b] moves to b', ..., until some row moves into ci); next[b] = that first b'
-    for (int b = 0; b < n; ++b) {
+    for (int b : alive) {
       dist[b] = INF;
       done[b] = 0;
       next[b] = -1;
     }
     dist[ci] = 0.0;
-    for (int it = 0; it < n - i; ++it) {
-      int bmin = -1;
+    // open = alive columns not yet finalised (compacted as they are finalised)
+    open.assign(alive.begin(), alive.end());
+    while (!open.empty()) {
+      int at = -1;
       double best = INF;
-      for (int b = 0; b < n; ++b)
-        if (col_alive[b] && !done[b] && dist[b] < best) {
-          best = dist[b];
-          bmin = b;
+      for (int q = 0; q < (int)open.size(); ++q)
+        if (dist[open[q]] < best) {
+          best = dist[open[q]];
+          at = q;
         }
-      if (bmin < 0) break;
+      if (at < 0) break;
+      const int bmin = open[at];
+      open[at] = open.back();
+      open.pop_back();
       done[bmin] = 1;
-      // a row r = row_of[b] (b != ci) may vacate b by moving into bmin
-      for (int b = 0; b < n; ++b) {
-        if (!col_alive[b] || done[b] || b == ci) continue;
-        const int r = row_of[b];
-        const double nd = best + (C[(int64_t)r * n + bmin] - u[r] - v[bmin]);
+      // a row r (unfixed, r != i) may vacate its column b = col_of[r] by moving into bmin;
+      // rows are walked in order so column bmin of C is read contiguously from CT
+      const double* ct = CT.data() + (size_t)bmin * n;
+      const double vb = v[bmin];
+      for (int r = i + 1; r < n; ++r) {
+        const int b = col_of[r];
+        if (done[b]) continue;
+        const double nd = best + (ct[r] - u[r] - vb);
         if (nd < dist[b]) {
           dist[b] = nd;
           next[b] = bmin;
@@ -214,6 +228,7 @@ extern "C" int hinm_lex_assignment(const double* C, int n, int64_t* assignment) 
     assignment[i] = jsel;
     prefix += C[(int64_t)i * n + jsel];
     col_alive[jsel] = 0;
+    alive.erase(std::find(alive.begin(), alive.end(), jsel));
   }
   return HINM_OK;
 }
