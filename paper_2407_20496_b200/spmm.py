@@ -149,17 +149,16 @@ def shuffle_encoding(enc: HiNMEncoding, rng) -> HiNMEncoding:
     return HiNMEncoding(shape=enc.shape, config=enc.config, sigma_o=enc.sigma_o, tiles=tiles)
 
 
-def _product_f32(enc: HiNMEncoding, X):
-    """fp32-output product of an encoding on the GPU (CUDA-core kernel; validation use)."""
-    torch = _torch()
-    pack = pack_from_encoding_nocache(enc, X.device)
-    return _spmm_simt(pack, X, order="sigma").double()
-
-
-def pack_from_encoding_nocache(enc, device):
+def _fresh_pack(enc, device):
+    """Device pack of an encoding, not cached on it (shuffled encodings are one-shot)."""
     from .pruning import pack_from_encoding
 
     return pack_from_encoding(enc, device)
+
+
+def _product_f32(enc: HiNMEncoding, X):
+    """fp32-output product of an encoding on the GPU (CUDA-core kernel; validation use)."""
+    return _spmm_simt(_fresh_pack(enc, X.device), X, order="sigma").double()
 
 
 def tile_shuffle_check(enc: HiNMEncoding, inputs, rng, trials: int = 50,
@@ -181,14 +180,14 @@ def tile_shuffle_check(enc: HiNMEncoding, inputs, rng, trials: int = 50,
     base_triples = kept_triples(enc)
     tc_ok = spmm_supported(enc.config.vector_size, enc.config.nm_keep, enc.config.nm_group)
     if tc_ok:
-        base_tc = torch.as_tensor(hinm_spmm(pack_from_encoding_nocache(enc, dev), X)).double()
+        base_tc = torch.as_tensor(hinm_spmm(_fresh_pack(enc, dev), X)).double()
     errors, tc_errors, kept_equal = [], [], True
     for _ in range(trials):
         sh = shuffle_encoding(enc, rng)
         kept_equal = kept_equal and (kept_triples(sh) == base_triples)
         errors.append(relative_error(_product_f32(sh, X).cpu().numpy(), base.cpu().numpy()))
         if tc_ok:
-            y = torch.as_tensor(hinm_spmm(pack_from_encoding_nocache(sh, dev), X)).double()
+            y = torch.as_tensor(hinm_spmm(_fresh_pack(sh, dev), X)).double()
             tc_errors.append(relative_error(y.cpu().numpy(), base_tc.cpu().numpy()))
     max_err = max(errors) if errors else 0.0
     return {"trials": trials, "kept_sets_equal": bool(kept_equal), "max_relative_error": max_err,
