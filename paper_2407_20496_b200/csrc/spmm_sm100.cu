@@ -32,18 +32,21 @@
 namespace hinm {
 namespace sm100 {
 
-constexpr int BN = 256;                        // tokens per unit (UMMA N)
+// Tokens per unit (UMMA N), a template parameter BNT of the kernel: 256 (one accumulator; the
+// default) or 128 (two accumulators so the next unit's MMAs overlap this unit's drain; an
+// experiment, see hinm_spmm_bf16).
 constexpr int BK = 64;                         // logical K per A / metadata stage (2 MMAs)
 constexpr int MAX_ASTAGES = 12;                // compressed-A / metadata ring (own barriers)
 // Gathered-X ring: KS K-rows (x 256 tokens) per stage.  The cp.async gather pays a fixed
 // per-stage cost in every producer warp (barrier wait + arrive), so 128-row stages
 // (16 warps x 8 rows) stream markedly faster than 64-row ones (scripts/l2_ring.cu on B200:
 // 20.4 vs 16.6 TB/s).
-__host__ __device__ constexpr int b_stages(int KS) { return KS == 128 ? 3 : 5; }
-__host__ __device__ constexpr int b_stage_bytes(int KS) { return KS * BN * 2; }
+__host__ __device__ constexpr int b_stages(int KS, int BNT) { return (KS == 128 ? 3 : 5) * (256 / BNT); }
+__host__ __device__ constexpr int b_stage_bytes(int KS, int BNT) { return KS * BNT * 2; }
+constexpr int MAX_XSTAGES = 10;
 constexpr int E_STAGE = 128 * 16;              // 128 lanes x 16 B metadata image per stage slot
 constexpr int TMEM_COLS = 512;
-constexpr int E_COL = 256;                     // metadata ring after the 256-column accumulator
+constexpr int E_COL = 256;                     // metadata ring after the accumulator(s)
 constexpr int E_SLOTS = 4;
 constexpr uint32_t META_PAD = 0x44444444u;     // 2:4 nibble {0,1} for rows >= V
 
@@ -72,18 +75,18 @@ struct SmemLayout {
 // cp.async gather under load, and with a shared barrier they held every X stage hostage
 // (scripts/l2_ring.cu).  One A stage covers one X stage (KS logical K: V*KS bytes of compressed
 // values + one metadata slot); depth = whatever fits next to the X ring.
-__host__ __device__ inline SmemLayout smem_layout(int V, int KS, bool m64) {
+__host__ __device__ inline SmemLayout smem_layout(int V, int KS, bool m64, int BNT) {
   SmemLayout L;
   const uint32_t slack = m64 ? 0 : 4096;       // M=128 descriptor over-read past V rows
   const uint32_t budget = 227 * 1024 - 1024 - 512 - slack;
   const uint32_t per = V * KS + E_STAGE;
-  const uint32_t xring = b_stages(KS) * b_stage_bytes(KS);
+  const uint32_t xring = b_stages(KS, BNT) * b_stage_bytes(KS, BNT);
   const uint32_t fit = (budget - xring) / per;
   L.ast = fit < (uint32_t)MAX_ASTAGES ? fit : MAX_ASTAGES;
   L.a = xring;
   L.e = L.a + L.ast * V * KS + slack;
   L.bar = L.e + L.ast * E_STAGE;
-  L.tmem = L.bar + (2 * 5 + 2 * MAX_ASTAGES + 2) * 8;
+  L.tmem = L.bar + (2 * MAX_XSTAGES + 2 * MAX_ASTAGES + 4) * 8;
   L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
   return L;
 }
@@ -239,13 +242,13 @@ __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc)
 
 // 16 lanes x (32 + 32) columns: thread l < 16 gets lane l, columns c..c+31; thread l >= 16 gets
 // lane l-16, columns c+128..c+159.
-template <bool WAIT = true>
+template <bool WAIT = true, int SPLIT = 128>
 __device__ __forceinline__ void tmem_ld_16x32bx2_x32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {"
-      "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 128;"
+      "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
+      : "r"(taddr), "n"(SPLIT));
   if (WAIT) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
@@ -272,6 +275,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32
 // B200: 8 warps/SM 15.6 TB/s, 12 -> 19.2, 16 -> 21.0 TB/s at any depth), so the default runs
 // 16 gather warps.
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant (column halves)
+static_assert(EPI_WARPS == 8, "epilogue warps: quadrant = warp & 3, column half = warp >> 2");
 constexpr int MMA_WARP = 8;
 constexpr int AE_WARP = 9;
 constexpr int GATHER_WARP0 = 10;
@@ -313,23 +317,26 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
 // M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
-template <int KS, int GW, int DBG = 0, bool M64 = false>
+template <int KS, int GW, int DBG = 0, bool M64 = false, int BNT = 256>
 __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     k_hinm_spmm(const uint16_t* __restrict__ X, int64_t ldx, Params p) {
   constexpr int NT = 32 * (GATHER_WARP0 + GW);
-  constexpr int STAGES = b_stages(KS), B_STAGE = b_stage_bytes(KS);
+  constexpr int STAGES = b_stages(KS, BNT), B_STAGE = b_stage_bytes(KS, BNT);
+  constexpr int NCHUNK = BNT / 64;            // 64-token SWIZZLE_128B chunks of a stage
+  constexpr int NACC = BNT == 128 ? 2 : 1;    // accumulators (TMEM columns 0 and 128)
+  static_assert(STAGES <= MAX_XSTAGES, "X ring");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const SmemLayout L = smem_layout(p.V, KS, M64);
+  const SmemLayout L = smem_layout(p.V, KS, M64, BNT);
   const int V = p.V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
   const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
   const uint32_t bar_afull = bar_empty + STAGES * 8, bar_aempty = bar_afull + MAX_ASTAGES * 8;
-  const uint32_t bar_acc_full = bar_aempty + MAX_ASTAGES * 8;
-  const uint32_t bar_acc_empty = bar_acc_full + 8;
+  const uint32_t bar_acc_full = bar_aempty + MAX_ASTAGES * 8;   // [NACC]
+  const uint32_t bar_acc_empty = bar_acc_full + 16;             // [NACC]
   const int AST = (int)L.ast;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
   // TMEM lane quadrants that hold real rows; two epilogue warps (column halves) per quadrant
@@ -355,8 +362,10 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       mbar_init(bar_afull + 8 * s, 1);
       mbar_init(bar_aempty + 8 * s, 1);
     }
-    mbar_init(bar_acc_full, 1);
-    mbar_init(bar_acc_empty, n_epi_warps);
+    for (int a = 0; a < NACC; ++a) {
+      mbar_init(bar_acc_full + 8 * a, 1);
+      mbar_init(bar_acc_empty + 8 * a, n_epi_warps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (j != slot) continue;
         r_ok[j] = pu < p.units;
         if (!r_ok[j]) return;
-        r_col[j] = pnb * BN;
+        r_col[j] = pnb * BNT;
         const int n = min(KS, pkp - ps * KS);
         r_n[j] = n;
         const int* gi = p.gidx + pk0 + ps * KS;
@@ -462,8 +471,12 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     };
 #pragma unroll
     for (int j = 0; j < PF; ++j) prefetch(j);
-    // per-warp constant part of the SWIZZLE_128B destination (row r = gw + GW i: r & 7 = gw & 7)
-    const uint32_t dst_lane = (lane >> 3) * (B_STAGE / 4) + gw * 128 + (((lane & 7) ^ (gw & 7)) << 4);
+    // A row segment is BNT tokens = LPR lanes x 16 B; one warp instruction covers RPI rows.
+    // Per-warp constant part of the SWIZZLE_128B destination (row r = gw + GW i: r & 7 = gw & 7)
+    constexpr int LPR = BNT / 8, RPI = 32 / LPR;
+    const int lpos = lane % LPR, rsub = lane / LPR;
+    const uint32_t dst_lane = (lpos >> 3) * (B_STAGE / NCHUNK) + (gw + rsub * GW) * 128 +
+                              (((lpos & 7) ^ (gw & 7)) << 4);
     const char* xbase = reinterpret_cast<const char*>(X);
     int stage = 0;
     uint32_t phase = 0;
@@ -474,7 +487,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (!r_ok[j]) { done = true; break; }
         // per row: SHFL + IMAD.WIDE + LDGSTS (the issue slots of the gather warps are the
         // scarce resource, ncu source view); rows < 64 always exist, the rest only in full stages
-        const int tok = r_col[j] + lane * 8;
+        const int tok = r_col[j] + lpos * 8;
         const uint32_t src_bytes = tok < p.B ? 16u : 0u;
         const char* xs = xbase + (src_bytes ? tok * 2 : 0);
         const uint32_t my_row = r_row[j];
@@ -482,10 +495,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
+        for (int k = 0; k < RPW / RPI; ++k) {
+          const int i = k * RPI + rsub;  // this lane's row (of the warp's RPW)
           const uint32_t row = __shfl_sync(0xffffffffu, my_row, i);
           if (DBG != 2 && (i * GW < 64 || full))
-            cp_async_16(dst0 + i * GW * 128, xs + (uint64_t)row * ldx2, src_bytes);  // IMAD.WIDE.U32
+            cp_async_16(dst0 + k * RPI * GW * 128, xs + (uint64_t)row * ldx2, src_bytes);  // IMAD.WIDE.U32
         }
         cp_async_arrive_noinc(bar_full + 8 * stage);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -498,11 +512,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     // registers); one elected lane issues the tcgen05 instructions.  A single-lane loop forced
     // R2UR conversions of every operand per MMA and measured 2.6x slower MMA issue
     // (scripts/mma_bench.cu vs mma_bench_v1.cu).
-    const uint32_t idesc = make_idesc(M64 ? 64 : 128, BN);
+    const uint32_t idesc = make_idesc(M64 ? 64 : 128, BNT);
     // descriptors at stage 0; the start-address field (16 B units, bits 0-13) is advanced by
     // adding byte offsets >> 4
     const uint64_t a_desc0 = smem_desc(sA, 128, 256, 0);
-    const uint64_t b_desc0 = smem_desc(sB, B_STAGE / 4, 1024, 2);
+    const uint64_t b_desc0 = smem_desc(sB, B_STAGE / NCHUNK, 1024, 2);
     const uint64_t e_desc0 = smem_desc(sE, 0, 128, 0);
     const uint32_t a_step = (uint32_t)(V * KS) >> 4, a_half = (uint32_t)(32 * V) >> 4;
     int stage = 0, aslot = 0;
@@ -512,9 +526,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       const int kp = nxt.kp;
       nxt = unit_params(p, u + gridDim.x);
       if (kp == 0) continue;
-      mbar_wait(bar_acc_empty, phase_acc_empty_parity(acc_uses));
+      const uint32_t acc = NACC == 2 ? (acc_uses & 1) : 0;
+      mbar_wait(bar_acc_empty + 8 * acc, phase_acc_empty_parity(acc_uses / NACC));
       ++acc_uses;
       tc_fence_after();
+      const uint32_t dtm = tmem + acc * BNT;
       const int nst = kp / BK;
       // one iteration per X stage (SUB = 1 or 2 A stages): all waits first, then one elected
       // block issues the metadata copy, 2 * SUB MMAs and the commits (the issue loop, not the
@@ -534,11 +550,11 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
           if (DBG != 1) {
-            mma_sp(tmem, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
-            mma_sp(tmem, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
+            mma_sp(dtm, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
+            mma_sp(dtm, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
             if (two) {
-              mma_sp(tmem, ad + 2 * a_half, bd + (8192 >> 4), idesc, ecol + 2, 1u);
-              mma_sp(tmem, ad + 3 * a_half, bd + (12288 >> 4), idesc | 1u, ecol + 2, 1u);
+              mma_sp(dtm, ad + 2 * a_half, bd + (8192 >> 4), idesc, ecol + 2, 1u);
+              mma_sp(dtm, ad + 3 * a_half, bd + (12288 >> 4), idesc | 1u, ecol + 2, 1u);
             }
           }
           tc_commit(bar_aempty + 8 * aslot);
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
-      if (elect_one()) tc_commit(bar_acc_full);
+      if (elect_one()) tc_commit(bar_acc_full + 8 * acc);
       __syncwarp();
     }
   } else {
@@ -558,15 +574,16 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     // its last load, before that chunk's bf16 conversion and stores.  The drain is the
     // critical path between consecutive units (the next unit's MMAs wait for it): with small K
     // it dominated the kernel (scripts/spmm_shape.py, HINM_GATHER=dbg_noepi), hence 8 warps.
-    //   M=64 : row 16q + (lane & 15); chunk c = columns 32c + 128(lane >= 16) + [0, 32),
-    //          c in {2h, 2h + 1}  (16x32bx2: lanes 0-15 of the quadrant hold the 16 rows)
-    //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c in [4h, 4h + 4)
+    //   M=64 : row 16q + (lane & 15); chunk c = columns 32c + (BNT/2)(lane >= 16) + [0, 32),
+    //          c in [h NCH, (h+1) NCH)  (16x32bx2: lanes 0-15 of the quadrant hold the 16 rows)
+    //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c in [h NCH, (h+1) NCH)
+    // With two accumulators (BNT = 128) the drain of one overlaps the MMAs into the other.
     const int q = warp & 3, h = warp >> 2;
     if (q < n_quads) {
       uint32_t ucount = 0;
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
-      const int c_own = M64 && lane >= 16 ? 128 : 0;
-      constexpr int NCH = M64 ? 2 : 4;  // chunks per warp
+      const int c_own = M64 && lane >= 16 ? BNT / 2 : 0;
+      constexpr int NCH = M64 ? BNT / 128 : BNT / 64;  // 32-column chunks per warp
       const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16) + h * NCH * 32;
       auto out_row = [&](const UnitParams& u) -> int64_t {
         const int64_t prow = (int64_t)u.t * V + r;
@@ -611,38 +628,48 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
         nxt = unit_params(p, u + gridDim.x);
         if (u + (int)gridDim.x < p.units) nxt_row = out_row(nxt);
         uint16_t* yrow = p.Y + orow * p.ldy;
-        const int col_base = cur.nb * BN + c_own + h * NCH * 32;
+        const int col_base = cur.nb * BNT + c_own + h * NCH * 32;
         if (cur.kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
           for (int c = 0; c < NCH * 4; ++c)
             if (col_base + c * 8 < p.B)
               *reinterpret_cast<uint4*>(yrow + col_base + c * 8) = make_uint4(0, 0, 0, 0);
           continue;
         }
-        mbar_wait(bar_acc_full, ucount & 1);
+        const uint32_t acc = NACC == 2 ? (ucount & 1) : 0;
+        mbar_wait(bar_acc_full + 8 * acc, (ucount / NACC) & 1);
         ++ucount;
         tc_fence_after();
+        const uint32_t t_acc = t_row + acc * BNT;
         if (DBG == 3) {  // experiment: release at once, no drain / stores
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acc_empty);
+          if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
+          continue;
+        }
+        uint32_t v0[32], v1[32];
+        if (NCH == 1) {  // one chunk per warp (M=64, BNT=128)
+          tmem_ld_16x32bx2_x32<true, BNT / 2>(t_acc, v0);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
+          store32(yrow, col_base, v0);
           continue;
         }
         // chunks are loaded in pairs (two tcgen05.ld in flight, one wait); the accumulator is
         // released after the last pair's wait
-        uint32_t v0[32], v1[32];
 #pragma unroll 1
         for (int c = 0; c < NCH; c += 2) {
           if (M64) {
-            tmem_ld_16x32bx2_x32<false>(t_row + c * 32, v0);
-            tmem_ld_16x32bx2_x32<false>(t_row + c * 32 + 32, v1);
+            tmem_ld_16x32bx2_x32<false, BNT / 2>(t_acc + c * 32, v0);
+            tmem_ld_16x32bx2_x32<false, BNT / 2>(t_acc + c * 32 + 32, v1);
           } else {
-            tmem_ld_32x32b_x32<false>(t_row + c * 32, v0);
-            tmem_ld_32x32b_x32<false>(t_row + c * 32 + 32, v1);
+            tmem_ld_32x32b_x32<false>(t_acc + c * 32, v0);
+            tmem_ld_32x32b_x32<false>(t_acc + c * 32 + 32, v1);
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (c + 2 == NCH) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_acc_empty);
+            if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
           }
           store32(yrow, col_base + c * 32, v0);
           store32(yrow, col_base + c * 32 + 32, v1);
@@ -701,19 +728,22 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   prm.B = B;
   prm.T = pk->T;
   prm.V = pk->V;
-  const int nbk = (B + BN - 1) / BN;
-  prm.units = nbk * pk->T;
   prm.out_order = out_order;
   static const int env_v8 = getenv("HINM_Y_V8") ? atoi(getenv("HINM_Y_V8")) : 1;
   prm.y_align32 = env_v8 && (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
-  const int grid = std::min(prm.units, sm_count());
   // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 contend
   // with the MMA for shared-memory bandwidth); V <= 64 -> 128-row X stages; V = 128 -> 64-row
   // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
-  // Experiments: HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128 (M=128 instruction for
-  // V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi (timing only: the results are garbage).
+  // Unit width BNT: 256 tokens.  BNT = 128 (two accumulators: the drain of one unit overlaps the
+  // next unit's MMAs, twice the units) is kept as an experiment: measured slower on every shape
+  // tried, small-K ones included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @ 802816
+  // 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is re-read
+  // twice as often, which outweighs the drain overlap.
+  // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128
+  // (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi (timing only).
   static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
   static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
+  static const int env_bn = getenv("HINM_BN") ? atoi(getenv("HINM_BN")) : 0;
   static const int variant = [] {
     const char* e = getenv("HINM_GATHER");
     if (!e) return 0;
@@ -723,10 +753,15 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_noepi")) return 4;
     return 0;
   }();
+  const int sms = sm_count();
+  int bnt = env_bn == 128 ? 128 : 256;
+  if (variant >= 2) bnt = 256;
+  prm.units = ((B + bnt - 1) / bnt) * pk->T;
+  const int grid = std::min(prm.units, sms);
   cudaStream_t st = (cudaStream_t)stream;
   const bool m64 = pk->V <= 64 && variant != 1;
-  auto launch = [&](auto kern, int ks, int gw) -> int {
-    const SmemLayout L = smem_layout(pk->V, ks, m64);
+  auto launch = [&](auto kern, int ks, int gw, int bn) -> int {
+    const SmemLayout L = smem_layout(pk->V, ks, m64, bn);
     HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(X, ldx, prm);
     return HINM_OK;
@@ -735,17 +770,22 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int gw = env_gw == 8 || env_gw == 16 ? env_gw : 8;
   int rc;
   if (variant == 2) {
-    rc = launch(k_hinm_spmm<128, 8, 1, true>, 128, 8);
+    rc = launch(k_hinm_spmm<128, 8, 1, true>, 128, 8, 256);
   } else if (variant == 3) {
-    rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8);
+    rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8, 256);
   } else if (variant == 4) {
-    rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8);
+    rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
+  } else if (bnt == 128) {
+    rc = ks == 128 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true, 128>, 128, 8, 128)
+                          : launch(k_hinm_spmm<128, 8, 0, false, 128>, 128, 8, 128))
+                   : (m64 ? launch(k_hinm_spmm<64, 8, 0, true, 128>, 64, 8, 128)
+                          : launch(k_hinm_spmm<64, 8, 0, false, 128>, 64, 8, 128));
   } else if (ks == 128) {
-    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true>, 128, 8) : launch(k_hinm_spmm<128, 8, 0, false>, 128, 8))
-                 : (m64 ? launch(k_hinm_spmm<128, 16, 0, true>, 128, 16) : launch(k_hinm_spmm<128, 16, 0, false>, 128, 16));
+    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true>, 128, 8, 256) : launch(k_hinm_spmm<128, 8, 0, false>, 128, 8, 256))
+                 : (m64 ? launch(k_hinm_spmm<128, 16, 0, true>, 128, 16, 256) : launch(k_hinm_spmm<128, 16, 0, false>, 128, 16, 256));
   } else {
-    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<64, 8, 0, true>, 64, 8) : launch(k_hinm_spmm<64, 8, 0, false>, 64, 8))
-                 : (m64 ? launch(k_hinm_spmm<64, 16, 0, true>, 64, 16) : launch(k_hinm_spmm<64, 16, 0, false>, 64, 16));
+    rc = gw == 8 ? (m64 ? launch(k_hinm_spmm<64, 8, 0, true>, 64, 8, 256) : launch(k_hinm_spmm<64, 8, 0, false>, 64, 8, 256))
+                 : (m64 ? launch(k_hinm_spmm<64, 16, 0, true>, 64, 16, 256) : launch(k_hinm_spmm<64, 16, 0, false>, 64, 16, 256));
   }
   if (rc) return rc;
   HINM_LAUNCH_CHECK();
