@@ -3,8 +3,8 @@ dense bf16 on the same shapes, plus the GPU compressor time.  One JSON document 
 
     python scripts/bench_configs.py [--quick] > profiles/r01_configs.json
 
-Timing: CUDA events around ITERS back-to-back launches after 3 warm-ups; inputs are resident in
-HBM.  Effective TFLOP/s = 2*m*n*tokens / t (the BASELINE.json metric).  Synthetic N(0,1) bf16
+Timing: CUDA events around ITERS back-to-back launches after 3 warm-ups and a 0.5 s pause (so
+neither arm runs power-capped); inputs are resident in HBM.  Effective TFLOP/s = 2*m*n*tokens / t (the BASELINE.json metric).  Synthetic N(0,1) bf16
 weights / activations, random sigma_o (seeded).
 """
 from __future__ import annotations
@@ -26,6 +26,10 @@ DEV = torch.device("cuda")
 
 
 def timed(fn, iters):
+    # start every measurement uncapped: sustained load engages the 1 kW power cap within ~0.1 s
+    # (SM clock 1965 -> ~1700 MHz, scripts/sustained_check.py); both arms get the same pause
+    torch.cuda.synchronize()
+    time.sleep(0.5)
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
