@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       for (int s = 0; s < nst; s += KS / BK) {             // one A stage per X stage
         mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
         const uint32_t fb = bar_afull + 8 * aslot;
-        if (elect_one()) {
+        if (DBG == 4) {  // experiment: no A / metadata loads at all
+          if (elect_one()) mbar_arrive(fb);
+        } else if (elect_one()) {
           const uint32_t a_bytes = V * 64 * min(KS / BK, nst - s);
           const uint32_t e_bytes = (s & 1) ? 0 : V * 16;   // metadata per 128-K block
           mbar_expect_tx(fb, a_bytes + e_bytes);
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
           const uint32_t ecol = tmem + E_COL + eslot * 4 + (s0 & 1) * 2;
           const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
-          if (DBG != 1) {
+          if (DBG != 1 && DBG != 4) {
             mma_sp(dtm, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
             mma_sp(dtm, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
             if (two) {
@@ -740,7 +742,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   // 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is re-read
   // twice as often, which outweighs the drain overlap.
   // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128
-  // (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi (timing only).
+  // (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi | dbg_gather_x_only
+  // (timing only: results are garbage).
   static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
   static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
   static const int env_bn = getenv("HINM_BN") ? atoi(getenv("HINM_BN")) : 0;
@@ -751,6 +754,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_nomma")) return 2;
     if (!strcmp(e, "dbg_nogather")) return 3;
     if (!strcmp(e, "dbg_noepi")) return 4;
+    if (!strcmp(e, "dbg_gather_x_only")) return 5;
     return 0;
   }();
   const int sms = sm_count();
@@ -775,6 +779,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8, 256);
   } else if (variant == 4) {
     rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
+  } else if (variant == 5) {
+    rc = launch(k_hinm_spmm<128, 8, 4, true>, 128, 8, 256);
   } else if (bnt == 128) {
     rc = ks == 128 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true, 128>, 128, 8, 128)
                           : launch(k_hinm_spmm<128, 8, 0, false, 128>, 128, 8, 128))
