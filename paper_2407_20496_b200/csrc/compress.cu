@@ -3,14 +3,15 @@
 // reduction reproduces numpy's summation order (see common.cuh / oracle/hinm_oracle.py).
 //
 // Kernels:
-//   k_scores      a3  col_score[t,j] = sum_r S[sigma_o[tV+r], j]  (fp64, sigma_o row order)
-//   (cub)         a4  per-tile stable descending sort of scores   (ties -> lower column)
-//   k_gains       a4  gains[t,q] = numpy-pairwise sum of M sorted scores
-//   k_budget      a5  global greedy == G smallest keys (-gain, q, t): threshold select
-//   k_survivors   a6/a7 ascending survivors per tile, vector mask
+//   k_scores4 / k_scores   a3  col_score[t,j] = sum_r S[sigma_o[tV+r], j]  (fp64, sigma_o order)
+//   k_tile_sort (cub for n > 16384)   a4  per-tile stable descending sort of the scores (ties ->
+//                      lower column), only over the key bits that differ inside the tile
+//   k_gains        a4  gains[t,q] = numpy-pairwise sum of M sorted scores (+ key OR / AND)
+//   k_budget_coop / k_budget_radix   a5  global greedy == G smallest keys (-gain, q, t)
+//   k_survivors    a6/a7 ascending survivors per tile, vector mask
 //   k_validate_sigma / k_dead_check   a7/a9 invariant checks (pruning.py:196-204, 226-254)
-//   k_nm_select   a8/a10 top-N per sigma_i group, reference view (nm_index, kept_values)
-//   k_pack_*      a10  operand image for the tcgen05 SpMM (padded gather index, UMMA A, E)
+//   k_select_pack  a8/a10 fused 2:4 select + reference view + tcgen05 operand image + gidx
+//   k_nm_select(_rows), k_pack_*   a8/a10 general N:M / V path and HiNMEncoding -> operand image
 #include <climits>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -189,97 +190,6 @@ __device__ int64_t block_sum64(int64_t v, int64_t* red) {
   int64_t out = *red;
   __syncthreads();
   return out;
-}
-
-// a5: the greedy allocator of pruning.py:99-129 as a threshold select over the merged key
-// lists.  Single block.  counts_cols[t] = M * (#selected groups of tile t).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_budget(const double* __restrict__ gains, int T, int G,
-                                               int64_t total_groups, int M,
-                                               int32_t* __restrict__ lo_scr,
-                                               int32_t* __restrict__ hi_scr,
-                                               int32_t* __restrict__ tile_ptr) {
-  __shared__ int64_t red;
-  // 1) smallest x with #{key <= x} >= total_groups
-  uint64_t lo = 0, hi = ~0ull;
-  while (lo < hi) {
-    uint64_t mid = lo + ((hi - lo) >> 1);
-    int64_t c = 0;
-    for (int t = threadIdx.x; t < T; t += NT) c += row_bound(gains + (int64_t)t * G, G, mid, true);
-    c = block_sum64<NT>(c, &red);
-    if (c >= total_groups) hi = mid; else lo = mid + 1;
-  }
-  const uint64_t xs = lo;
-  int64_t less = 0;
-  for (int t = threadIdx.x; t < T; t += NT) {
-    const double* row = gains + (int64_t)t * G;
-    int a = row_bound(row, G, xs, false), b = row_bound(row, G, xs, true);
-    lo_scr[t] = a;
-    hi_scr[t] = b;
-    less += a;
-  }
-  __syncthreads();
-  less = block_sum64<NT>(less, &red);
-  const int64_t R = total_groups - less;  // ties at key xs still to take, ordered by (q, t)
-  // 2) smallest Q with F(Q) = sum_t clamp(min(hi, Q+1) - lo, 0) >= R
-  int qlo = 0, qhi = G;  // Q in [0, G)
-  if (R > 0) {
-    qhi = G - 1;
-    while (qlo < qhi) {
-      int mid = (qlo + qhi) >> 1;
-      int64_t f = 0;
-      for (int t = threadIdx.x; t < T; t += NT) {
-        int v = min(hi_scr[t], mid + 1) - lo_scr[t];
-        f += v > 0 ? v : 0;
-      }
-      f = block_sum64<NT>(f, &red);
-      if (f >= R) qhi = mid; else qlo = mid + 1;
-    }
-  }
-  const int Q = qlo;
-  int64_t below = 0;
-  if (R > 0) {
-    for (int t = threadIdx.x; t < T; t += NT) {
-      int v = min(hi_scr[t], Q) - lo_scr[t];
-      below += v > 0 ? v : 0;
-    }
-    below = block_sum64<NT>(below, &red);
-  }
-  int64_t rem = R - below;  // tiles (in t order) with lo <= Q < hi that take one more
-  // 3) counts + exclusive prefix over tiles (chunked block scan)
-  typedef cub::BlockScan<int64_t, NT> BS;
-  __shared__ typename BS::TempStorage scan_tmp;
-  __shared__ int64_t carry_at, carry_ptr;
-  if (threadIdx.x == 0) { carry_at = 0; carry_ptr = 0; }
-  __syncthreads();
-  for (int base = 0; base < T; base += NT) {
-    int t = base + threadIdx.x;
-    int64_t at_q = 0, cnt = 0;
-    if (t < T) {
-      int l = lo_scr[t], h = hi_scr[t];
-      if (R > 0) {
-        int v = min(h, Q) - l;
-        cnt = l + (v > 0 ? v : 0);
-        at_q = (l <= Q && Q < h) ? 1 : 0;
-      } else {
-        cnt = l;
-      }
-    }
-    int64_t excl_at;
-    BS(scan_tmp).ExclusiveSum(at_q, excl_at);
-    __syncthreads();
-    if (at_q && carry_at + excl_at < rem) cnt += 1;
-    int64_t cols = cnt * M, excl_cols;
-    BS(scan_tmp).ExclusiveSum(cols, excl_cols);
-    __syncthreads();
-    if (t < T) tile_ptr[t] = (int32_t)(carry_ptr + excl_cols);
-    // chunk totals
-    int64_t tot_at = block_sum64<NT>(at_q, &red);
-    int64_t tot_cols = block_sum64<NT>(cols, &red);
-    if (threadIdx.x == 0) { carry_at += tot_at; carry_ptr += tot_cols; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) tile_ptr[T] = (int32_t)carry_ptr;
 }
 
 // a4 (fast path, n <= 16384): one CTA per tile sorts the tile's scores in registers/smem with a
@@ -893,22 +803,6 @@ __device__ __forceinline__ int64_t aval_offset(int64_t kofs_t, int V, int r, int
   const int b = kc >> 5, kcb = kc & 31, j = kcb >> 4, kcs = kcb & 15;
   return (kofs_t >> 1) * V + (int64_t)b * 32 * V + (int64_t)j * 16 * V + (r >> 3) * 128 +
          (kcs >> 3) * 64 + (r & 7) * 8 + (kcs & 7);
-}
-
-__global__ void k_pack_vals(const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ kofs,
-                            const uint16_t* __restrict__ kept, int V, int T, int64_t total_groups,
-                            uint16_t* __restrict__ a_vals) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= total_groups * V) return;
-  const int64_t g = gid / V;
-  const int r = (int)(gid % V);
-  const int t = tile_of_group(tile_ptr, T, 4, g);
-  const int64_t g_in = g - tile_ptr[t] / 4;
-  const int Gt = (tile_ptr[t + 1] - tile_ptr[t]) / 4;
-  const int64_t src = (int64_t)V * (tile_ptr[t] / 4) * 2 + (int64_t)r * Gt * 2 + g_in * 2;
-  const int64_t ko = kofs[t];
-  a_vals[aval_offset(ko, V, r, (int)(2 * g_in))] = kept[src];
-  a_vals[aval_offset(ko, V, r, (int)(2 * g_in + 1))] = kept[src + 1];
 }
 
 // 2:4 fast path: one thread writes one 16-byte core-matrix row (8 compressed values = 4 groups
