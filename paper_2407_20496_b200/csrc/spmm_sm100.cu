@@ -737,10 +737,10 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   // with the MMA for shared-memory bandwidth); V <= 64 -> 128-row X stages; V = 128 -> 64-row
   // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
   // Unit width BNT: 256 tokens.  BNT = 128 (two accumulators: the drain of one unit overlaps the
-  // next unit's MMAs, twice the units) is kept as an experiment: measured slower on every shape
-  // tried, small-K ones included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @ 802816
+  // next unit's MMAs, twice the units) is slower whenever the 256-token units fill the machine,
+  // small-K shapes included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @ 802816
   // 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is re-read
-  // twice as often, which outweighs the drain overlap.
+  // twice as often.  It is used only when the units would otherwise leave SMs idle.
   // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128
   // (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi | dbg_gather_x_only
   // (timing only: results are garbage).
@@ -758,7 +758,12 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     return 0;
   }();
   const int sms = sm_count();
-  int bnt = env_bn == 128 ? 128 : 256;
+  // 128-token units only when 256-token units would leave more than half the SMs idle (e.g. the
+  // down projection at 256 tokens per GPU under 8-way token sharding: 64 units -> 128 units,
+  // 0.030 -> 0.024 ms); with more units the 256-token kernel wins
+  const int64_t units256 = (int64_t)((B + 255) / 256) * pk->T;
+  int bnt = units256 * 2 <= sms ? 128 : 256;
+  if (env_bn == 128 || env_bn == 256) bnt = env_bn;
   if (variant >= 2) bnt = 256;
   prm.units = ((B + bnt - 1) / bnt) * pk->T;
   const int grid = std::min(prm.units, sms);
