@@ -278,7 +278,15 @@ constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant (column halves)
 static_assert(EPI_WARPS == 8, "epilogue warps: quadrant = warp & 3, column half = warp >> 2");
 constexpr int MMA_WARP = 8;
 constexpr int AE_WARP = 9;
-constexpr int GATHER_WARP0 = 10;
+// First gather warp.  With 8 gather warps the kernel runs 18 warps on the launch register budget.
+// With 16 (experiment HINM_GW=16) the 832+ threads would cap every role at 72 registers (the
+// epilogue and gather loops spilled, which is what made 16 warps look slower), so the gather
+// warps start on a warpgroup boundary (warp 12; warps 10-11 idle) and the warpgroups rebalance
+// registers with setmaxnreg: gather 16 x 56, epilogue 8 x 104.  Spill-free, it runs exactly as
+// fast as 8 warps (LLaMA up 0.741 vs 0.740 ms): under a running MMA the gather is capped by the
+// SM's L2->SMEM fill rate, not by issuing warps (scripts/mma_gather_contention.cu).
+__host__ __device__ constexpr int gather_warp0(int GW) { return GW == 8 ? 10 : 12; }
+constexpr int GATHER_REGS = 56, EPI_REGS = 104;
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -318,8 +326,10 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
 // M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
 template <int KS, int GW, int DBG = 0, bool M64 = false, int BNT = 256>
-__global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
+__global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     k_hinm_spmm(const uint16_t* __restrict__ X, int64_t ldx, Params p) {
+  constexpr int GATHER_WARP0 = gather_warp0(GW);
+  constexpr bool REBALANCE = GATHER_WARP0 % 4 == 0 && GW % 4 == 0;
   constexpr int NT = 32 * (GATHER_WARP0 + GW);
   constexpr int STAGES = b_stages(KS, BNT), B_STAGE = b_stage_bytes(KS, BNT);
   constexpr int NCHUNK = BNT / 64;            // 64-token SWIZZLE_128B chunks of a stage
@@ -421,6 +431,7 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
     }
   } else if (warp >= GATHER_WARP0) {
     // ============================================================ gather producers
+    if (REBALANCE) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(GATHER_REGS));
     // Flattened stream over (unit, X stage) with the gather indices of stage i+PF loaded while
     // stage i is issued (the dependent index load never sits on the critical path).  The
     // issue loop is kept to ~4 instructions per 512-byte row: warp gw owns the K-rows
@@ -569,8 +580,9 @@ __global__ void __launch_bounds__(32 * (GATHER_WARP0 + GW), 1)
       if (elect_one()) tc_commit(bar_acc_full + 8 * acc);
       __syncwarp();
     }
-  } else {
+  } else if (warp < EPI_WARPS) {
     // ============================================================ epilogue (warps 0-7)
+    if (REBALANCE) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
     // Warp w drains TMEM lane quadrant q = w & 3, column half h = w >> 2, with 32-column
     // tcgen05.ld's issued in pairs, and releases the accumulator to the MMA issuer right after
     // its last load, before that chunk's bf16 conversion and stores.  The drain is the
@@ -733,8 +745,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   prm.out_order = out_order;
   static const int env_v8 = getenv("HINM_Y_V8") ? atoi(getenv("HINM_Y_V8")) : 1;
   prm.y_align32 = env_v8 && (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
-  // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 contend
-  // with the MMA for shared-memory bandwidth); V <= 64 -> 128-row X stages; V = 128 -> 64-row
+  // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 are no
+  // faster: the fill rate under a running MMA is the cap); V <= 64 -> 128-row X stages; V = 128 -> 64-row
   // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
   // Unit width BNT: 256 tokens.  BNT = 128 (two accumulators: the drain of one unit overlaps the
   // next unit's MMAs, twice the units) is slower whenever the 256-token units fill the machine,
@@ -772,7 +784,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   auto launch = [&](auto kern, int ks, int gw, int bn) -> int {
     const SmemLayout L = smem_layout(pk->V, ks, m64, bn);
     HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<grid, 32 * (GATHER_WARP0 + gw), L.total, st>>>(X, ldx, prm);
+    kern<<<grid, 32 * (gather_warp0(gw) + gw), L.total, st>>>(X, ldx, prm);
     return HINM_OK;
   };
   const int ks = env_ks == 64 || env_ks == 128 ? env_ks : (pk->V <= 64 ? 128 : 64);
