@@ -88,3 +88,30 @@ def test_dropin_entry_points_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(H.DeviceError):
         H.vector_prune(np.ones((4, 8)), H.HiNMConfig(2, 1, 2, 0.5), np.arange(4))
+
+
+# values produced by the reference's hinm.model.count_permutation_space (model.py:249-267);
+# the large case is pinned by its bit length and its residue mod 2**61 - 1
+@pytest.mark.parametrize("args,exact,residue,bits", [
+    ((8, 8, 4, 4), 2450, 2450, 12),
+    ((16, 32, 4, 4), 623138617594693176539062500, 420383145671866053, 90),
+    ((6, 8, 2, 2), 4725, 4725, 13),
+    ((4, 4, 1, 1), 4, 4, 3),
+    ((768, 3072, 64, 4), None, 206401976091169948, 24066),
+])
+def test_count_permutation_space(args, exact, residue, bits):
+    v = H.count_permutation_space(*args)
+    if exact is not None:
+        assert v == exact
+    assert v % (2 ** 61 - 1) == residue and v.bit_length() == bits
+
+
+@pytest.mark.parametrize("args", [(0, 4, 1, 1), (6, 8, 4, 2), (8, 6, 4, 4)])
+def test_count_permutation_space_errors(args):
+    with pytest.raises(H.DimensionError):
+        H.count_permutation_space(*args)
+
+
+def test_reference_names_exported():
+    for name in ("Partition", "ScheduleState", "assignment_cost", "count_permutation_space"):
+        assert name in H.__all__ and hasattr(H, name)
