@@ -2,7 +2,7 @@
 small-K cfg4 layers), CUDA-graph replays of ITERS calls so host launch overhead is excluded.
 Kernel variants are selected with the HINM_* environment switches of hinm_spmm_bf16.
 
-    python scripts/small_shapes.py [--cublas]
+    python scripts/small_shapes.py [--cublas] [--sigma]
 """
 from __future__ import annotations
 
@@ -50,6 +50,7 @@ def graph_time(fn, iters=ITERS):
 
 def main():
     cublas = "--cublas" in sys.argv
+    order = "sigma" if "--sigma" in sys.argv else "original"
     tag = {k: v for k, v in os.environ.items() if k.startswith("HINM_")}
     for m, n, tok in SHAPES:
         g = torch.Generator(device=DEV).manual_seed(0)
@@ -57,11 +58,12 @@ def main():
         X = torch.randn(n, tok, generator=g, device=DEV).to(torch.bfloat16)
         Y = torch.empty(m, tok, dtype=torch.bfloat16, device=DEV)
         pack = H.compress(W, H.HiNMConfig(64, 2, 4, 0.5), np.random.default_rng(0).permutation(m))
-        row = {"shape": f"{m}x{n}@{tok}", "spmm_us": round(graph_time(lambda: H.spmm(pack, X, out=Y, order="original")), 2)}
+        row = {"shape": f"{m}x{n}@{tok}", "spmm_us": round(graph_time(lambda: H.spmm(pack, X, out=Y, order=order)), 2)}
         if cublas:
             Yc = torch.empty(m, tok, dtype=torch.bfloat16, device=DEV)
             row["cublas_us"] = round(graph_time(lambda: torch.matmul(W, X, out=Yc)), 2)
         row.update(tag)
+        row["order"] = order
         print(json.dumps(row), flush=True)
         del W, X, Y, pack
         torch.cuda.empty_cache()
