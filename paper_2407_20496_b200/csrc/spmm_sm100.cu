@@ -791,7 +791,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int gw = env_gw == 8 || env_gw == 16 ? env_gw : 8;
   int rc;
   if (variant == 2) {
-    rc = launch(k_hinm_spmm<128, 8, 1, true>, 128, 8, 256);
+    rc = gw == 16 ? launch(k_hinm_spmm<128, 16, 1, true>, 128, 16, 256) : launch(k_hinm_spmm<128, 8, 1, true>, 128, 8, 256);
   } else if (variant == 3) {
     rc = launch(k_hinm_spmm<128, 8, 2, true>, 128, 8, 256);
   } else if (variant == 4) {
