@@ -27,6 +27,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace hinm {
@@ -390,6 +393,12 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const int T = p.T;
+  // Programmatic dependent launch: everything above (barrier init, TMEM allocation, metadata pad)
+  // touches only this CTA's shared memory / TMEM, so it overlaps the previous kernel's tail; no
+  // global memory is read or written before the previous grid has completed.  The next kernel
+  // may start its own prologue as soon as this grid's CTAs start exiting.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == AE_WARP) {
     // ============================================================ A / metadata producer
@@ -707,11 +716,47 @@ namespace {
 
 thread_local int g_last_launches = 0;
 
-int sm_count() {
-  int dev = 0, n = 0;
+// Per-device SM count and per-(kernel, device) shared-memory opt-in, cached: the launch path is
+// on the critical path of short SpMMs (host time per call, scripts/host_overhead.py).
+constexpr int MAX_DEVICES = 64;
+int g_sms[MAX_DEVICES] = {};
+
+int current_device() {
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  return dev;
+}
+
+int sm_count(int dev) {
+  if (dev < 0 || dev >= MAX_DEVICES) return 148;
+  if (g_sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n > 0 ? n : 148;
+  }
+  return g_sms[dev];
+}
+
+struct SmemOptIn {
+  const void* fn;
+  int dev;
+  int bytes;
+};
+std::mutex g_optin_mu;
+std::vector<SmemOptIn> g_optin;
+
+cudaError_t ensure_smem(const void* fn, int dev, int bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_optin_mu);
+    for (const SmemOptIn& o : g_optin)
+      if (o.fn == fn && o.dev == dev && o.bytes >= bytes) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_optin_mu);
+    g_optin.push_back({fn, dev, bytes});
+  }
+  return e;
 }
 
 }  // namespace
@@ -769,7 +814,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_gather_x_only")) return 5;
     return 0;
   }();
-  const int sms = sm_count();
+  const int dev = current_device();
+  const int sms = sm_count(dev);
   // 128-token units only when 256-token units would leave more than half the SMs idle (e.g. the
   // down projection at 256 tokens per GPU under 8-way token sharding: 64 units -> 128 units,
   // 0.030 -> 0.024 ms); with more units the 256-token kernel wins
@@ -781,10 +827,26 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int grid = std::min(prm.units, sms);
   cudaStream_t st = (cudaStream_t)stream;
   const bool m64 = pk->V <= 64 && variant != 1;
+  // Short kernels are launched with programmatic stream serialization (PDL): back-to-back SpMMs
+  // (layer chains, CUDA graphs) overlap this kernel's prologue with the previous kernel's tail,
+  // ~1-1.7 us per launch on the BERT / cfg1 shapes (scripts/small_shapes.py).  Long kernels (more
+  // than 8 units per SM) gain nothing measurable and keep plain launches (HINM_PDL = 0 | 1 forces).
+  static const int env_pdl = getenv("HINM_PDL") ? atoi(getenv("HINM_PDL")) : -1;
+  const bool pdl = env_pdl == 1 || (env_pdl == -1 && prm.units <= 8 * sms);
   auto launch = [&](auto kern, int ks, int gw, int bn) -> int {
     const SmemLayout L = smem_layout(pk->V, ks, m64, bn);
-    HINM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    kern<<<grid, 32 * (gather_warp0(gw) + gw), L.total, st>>>(X, ldx, prm);
+    HINM_CUDA_TRY(ensure_smem((const void*)kern, dev, (int)L.total));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32 * (gather_warp0(gw) + gw));
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    HINM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, X, ldx, prm));
     return HINM_OK;
   };
   const int ks = env_ks == 64 || env_ks == 128 ? env_ks : (pk->V <= 64 ? 128 : 64);

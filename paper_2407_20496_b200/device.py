@@ -24,7 +24,12 @@ def _torch():
 
 
 def _stream_handle(device=None) -> int:
+    """torch's current CUDA stream on ``device`` (raw cudaStream_t)."""
     torch = _torch()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:  # ~10x cheaper than current_stream() on the per-call launch path
+        idx = device.index if hasattr(device, "index") else device
+        return raw(torch.cuda.current_device() if idx is None else idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -75,7 +80,17 @@ class DevicePack:
     def shape(self) -> tuple[int, int]:
         return (self.m, self.n)
 
+    def __setattr__(self, name, value):
+        # any field change invalidates the cached C view of the pack
+        object.__setattr__(self, name, value)
+        if name != "_struct_cache":
+            object.__setattr__(self, "_struct_cache", None)
+
     def struct(self) -> _lib.PackStruct:
+        """The C-ABI view (hinm_pack_t) of this pack; cached until a field is reassigned."""
+        cached = self.__dict__.get("_struct_cache")
+        if cached is not None:
+            return cached
         s = _lib.PackStruct()
         s.m, s.n, s.V, s.N, s.M, s.T = self.m, self.n, self.V, self.N, self.M, self.T
         s.total_keep = self.total_keep
@@ -84,6 +99,7 @@ class DevicePack:
         s.kpad_cap, s.meta_words_cap = self.kpad_cap, self.meta_cap
         s.tile_kofs, s.tile_eofs = _ptr(self.tile_kofs), _ptr(self.tile_eofs)
         s.gidx, s.a_vals, s.a_meta = _ptr(self.gidx), _ptr(self.a_vals), _ptr(self.a_meta)
+        object.__setattr__(self, "_struct_cache", s)
         return s
 
     @property

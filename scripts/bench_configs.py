@@ -42,7 +42,32 @@ def timed(fn, iters):
     return s.elapsed_time(e) / iters
 
 
-def gemm_case(m, n, tokens, V, sv, seed, iters, cublas_cache=None):
+def graph_timed(fn, iters):
+    """GPU-side time per call: one CUDA graph holding `iters` back-to-back calls (no host launch
+    overhead in either arm; the HiNM launches keep their programmatic-dependent-launch edges)."""
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(iters):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    time.sleep(0.5)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def gemm_case(m, n, tokens, V, sv, seed, iters, cublas_cache=None, graph=False):
     if os.environ.get("EMPTY_CACHE"):
         torch.cuda.empty_cache()
     g = torch.Generator(device=DEV).manual_seed(seed)
@@ -66,18 +91,31 @@ def gemm_case(m, n, tokens, V, sv, seed, iters, cublas_cache=None):
         if cublas_cache is not None:
             cublas_cache[key] = cb
     f = 2.0 * m * n * tokens
-    return {"m": m, "n": n, "tokens": tokens, "V": V, "s_v": sv, "spmm_ms": round(ms, 4),
-            "cublas_ms": round(cb, 4), "speedup": round(cb / ms, 3),
-            "eff_tflops": round(f / ms / 1e9, 1), "cublas_tflops": round(f / cb / 1e9, 1),
-            "compress_ms": round(comp_ms, 3)}
+    row = {"m": m, "n": n, "tokens": tokens, "V": V, "s_v": sv, "spmm_ms": round(ms, 4),
+           "cublas_ms": round(cb, 4), "speedup": round(cb / ms, 3),
+           "eff_tflops": round(f / ms / 1e9, 1), "cublas_tflops": round(f / cb / 1e9, 1),
+           "compress_ms": round(comp_ms, 3)}
+    if graph:  # latency-bound shapes: eager timing above is host-launch bound in both arms
+        Yc = torch.empty(m, tokens, dtype=torch.bfloat16, device=DEV)
+        gs = graph_timed(lambda: H.spmm(pack, X, out=Y, order="original"), 40)
+        gc = graph_timed(lambda: torch.matmul(W, X, out=Yc), 40)
+        row.update({"spmm_graph_ms": round(gs, 4), "cublas_graph_ms": round(gc, 4),
+                    "speedup_graph": round(gc / gs, 3)})
+    return row
 
 
 def summarize(rows, label):
     sp = sum(r["spmm_ms"] * r.get("count", 1) for r in rows)
     cb = sum(r["cublas_ms"] * r.get("count", 1) for r in rows)
     fl = sum(2.0 * r["m"] * r["n"] * r["tokens"] * r.get("count", 1) for r in rows)
-    return {"config": label, "spmm_ms_total": round(sp, 3), "cublas_ms_total": round(cb, 3),
-            "speedup": round(cb / sp, 3), "eff_tflops": round(fl / sp / 1e9, 1)}
+    out = {"config": label, "spmm_ms_total": round(sp, 3), "cublas_ms_total": round(cb, 3),
+           "speedup": round(cb / sp, 3), "eff_tflops": round(fl / sp / 1e9, 1)}
+    if all("spmm_graph_ms" in r for r in rows):
+        gs = sum(r["spmm_graph_ms"] * r.get("count", 1) for r in rows)
+        gc = sum(r["cublas_graph_ms"] * r.get("count", 1) for r in rows)
+        out.update({"spmm_graph_ms_total": round(gs, 3), "cublas_graph_ms_total": round(gc, 3),
+                    "speedup_graph": round(gc / gs, 3)})
+    return out
 
 
 def main():
@@ -102,14 +140,15 @@ def main():
 
     # cfg1: BERT-base FFN 768x3072 (and the transposed reading 3072x768), 512 tokens
     if want("cfg1"):
-      rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache), gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache)]
+      rows = [gemm_case(768, 3072, 512, 64, 0.5, 1, 50, cache, graph=True),
+              gemm_case(3072, 768, 512, 64, 0.5, 1, 50, cache, graph=True)]
       out["cfg1"] = {"rows": rows, "note": "launch/latency bound (2.4 GFLOP); the CPU reference path "
                    "for this config is bench.py --impl reference / cpu_baseline"}
 
     # cfg2: BERT-base, 12 layers x (Q, K, V, O 768x768; FFN1 3072x768; FFN2 768x3072), 4096 tokens
     rows = []
     for nm, m, n, cnt in () if not want("cfg2") else (("qkvo", 768, 768, 48), ("ffn1", 3072, 768, 12), ("ffn2", 768, 3072, 12)):
-        r = gemm_case(m, n, 4096, 64, 0.5, 11, it, cache)
+        r = gemm_case(m, n, 4096, 64, 0.5, 11, it, cache, graph=True)
         r.update({"layer": nm, "count": cnt})
         rows.append(r)
     if rows:
