@@ -4,8 +4,10 @@ Workload (BASELINE.json configs[2], the headline target): one LLaMA-7B FFN layer
 sparsity (V=64, 2:4, s_v=0.5) on 16384 tokens -- gate + up (11008x4096) and down
 (4096x11008) SpMMs per step, the down projection consuming the up projection's output in
 original channel order (the sigma_o restore is fused in the epilogue).  Token-sharded over N
-GPUs with replicated packed weights and no collective in the timed region (strong scaling:
-global tokens fixed).  Synthetic N(0,1) bf16 weights/activations, seeded; random sigma_o.
+GPUs with replicated packed weights and no collective in the timed region.  Weak scaling by
+default (the path partitions into independent token shards): every rank runs the 16384-token
+workload on its own shard, so N ranks process N x 16384 tokens; --strong keeps 16384 global
+tokens split N ways.  Synthetic N(0,1) bf16 weights/activations, seeded; random sigma_o.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -138,7 +140,9 @@ def run_ours(args):
         dist.barrier()
     lib = _lib.load()
 
-    tokens = GLOBAL_TOKENS // world                      # token shard of this rank
+    # token shard of this rank: weak scaling (default) keeps 16384 tokens per rank
+    global_tokens = GLOBAL_TOKENS if args.strong else GLOBAL_TOKENS * world
+    tokens = global_tokens // world
     cfg = H.HiNMConfig(V, NM_N, NM_M, SV)
     g = torch.Generator(device=dev)
     packs, dense = {}, {}
@@ -209,7 +213,7 @@ def run_ours(args):
     launches = 3 * args.steps                            # hinm_spmm_bf16 launches one kernel each
     assert lib.hinm_last_launch_count() == 1
     ms_step = ms_total / args.steps
-    value = eff_flops(GLOBAL_TOKENS) / (ms_step * 1e-3) / 1e12
+    value = eff_flops(global_tokens) / (ms_step * 1e-3) / 1e12
 
     # cuBLAS dense comparator on the same shapes, measured the same way as our step (W warm-up
     # steps, K timed steps of the three GEMMs back to back, per-GEMM events) after a 1 s pause:
@@ -236,7 +240,7 @@ def run_ours(args):
     cublas = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in ev) / args.steps for j, nm in enumerate(names)}
     ev = None
     ms_cublas_step = sum(cublas.values())
-    cublas_tflops = eff_flops(GLOBAL_TOKENS) / (ms_cublas_step * 1e-3) / 1e12
+    cublas_tflops = eff_flops(global_tokens) / (ms_cublas_step * 1e-3) / 1e12
 
     # end to end through the public API (HostChain -> hinm_chain_run_host): pinned host X in,
     # Y_down out, every step; H2D / SpMMs / D2H of consecutive token chunks overlap
@@ -260,7 +264,7 @@ def run_ours(args):
         return
     pk, kind = peaks()
     p_sparse = 2.0 * pk["bf16_tflops"]
-    f_sp = sparse_flops(GLOBAL_TOKENS // world)
+    f_sp = sparse_flops(tokens)
     achieved = f_sp / (sum(per_kernel.values()) * 1e-3) / 1e12
     # the gather roofline: every kept K-row of a tile is streamed L2 -> SMEM once per 256-token
     # block (2 * T * k_bar * tokens bytes) plus the compressed A / metadata image per unit
@@ -287,14 +291,15 @@ def run_ours(args):
         "ms_per_step": round(ms_step, 4),
         "ms_per_step_p10_p50_p90": [round(pct(0.1), 4), round(pct(0.5), 4), round(pct(0.9), 4)],
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 weights/activations, random sigma_o)",
         "config": {
             "workload": "LLaMA-7B FFN layer (gate+up 11008x4096, down 4096x11008), 75% HiNM "
-                        "V=64 2:4 s_v=0.5, 16384 tokens token-sharded",
-            "global_tokens": GLOBAL_TOKENS, "tokens_per_gpu": GLOBAL_TOKENS // world,
+                        "V=64 2:4 s_v=0.5, " + ("16384 tokens token-sharded" if args.strong else
+                                                "16384 tokens per GPU, token-sharded"),
+            "global_tokens": global_tokens, "tokens_per_gpu": tokens,
             "parallelism": f"token-shard x{world}, weights replicated, no collective",
             "l2": "inputs larger than L2 (X 134 MB + 3 packs ~150 MB per step at N=1)",
         },
@@ -327,7 +332,7 @@ def run_ours(args):
                                                 / pk["hbm_gbs"], 4),
                        "note": "ms: host wall per layer incl. allocation + sigma validation sync; "
                                "stream_ms: CUDA events around the call; 3 layers"},
-        "e2e": {"value": round(eff_flops(GLOBAL_TOKENS) / (ms_e2e * 1e-3) / 1e12, 2),
+        "e2e": {"value": round(eff_flops(global_tokens) / (ms_e2e * 1e-3) / 1e12, 2),
                 "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2),
                 "path": f"HostChain (hinm_chain_run_host), {chunk}-token chunks, pinned host buffers"},
@@ -408,7 +413,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": "LLaMA-7B FFN down projection sample (4096x11008, V=64 2:4, "
                                f"{tokens} tokens) of the bench workload"},
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
@@ -428,6 +434,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-tokens", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: 16384 global tokens split over the ranks (default: weak, "
+                         "16384 tokens per rank)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
