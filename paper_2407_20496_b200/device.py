@@ -188,7 +188,7 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
     m, n = weights.shape
     vcfg = ensure_validated(cfg, (m, n))
     dev = weights.device
-    so = torch.as_tensor(np.asarray(sigma_o), dtype=torch.int32).to(dev) if not (
+    so = torch.from_numpy(np.ascontiguousarray(sigma_o, dtype=np.int32)).to(dev) if not (
         hasattr(sigma_o, "is_cuda")) else sigma_o.to(device=dev, dtype=torch.int32)
     if so.numel() != m:
         raise ShapeMismatch(f"sigma_o has {so.numel()} entries, weights have {m} rows")
