@@ -35,7 +35,7 @@ constexpr int SB = 65536, SA = 16384, SG = 131072;
 // SPARSE: 1 = sparse M=64 N=256 K=32, 0 = dense M=128 N=256 K=16; do_mma = 0: gather alone
 template <int SPARSE>
 __global__ void bench(const uint4* __restrict__ src, const int* __restrict__ idx, int iters, int do_mma,
-                      unsigned long long* out) {
+                      unsigned long long* out, int gap_cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -90,6 +90,11 @@ __global__ void bench(const uint4* __restrict__ src, const int* __restrict__ idx
           }
         }
         __syncwarp();
+        // duty < 100 %: after each batch of 8 MMAs, hold the issue for gap_cycles
+        if (gap_cycles) {
+          const long long tg = clock64();
+          while (clock64() - tg < gap_cycles) {}
+        }
       }
       if (elect_one())
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
@@ -140,12 +145,13 @@ __global__ void bench(const uint4* __restrict__ src, const int* __restrict__ idx
 }
 
 template <int SPARSE>
-void run(const uint4* src, const int* idx, int gwarps, int do_mma, int sms, unsigned long long* d) {
+void run(const uint4* src, const int* idx, int gwarps, int do_mma, int sms, unsigned long long* d,
+         int gap = 0) {
   const int iters = 16384;
   const int smem = SB + SA + SG;
   cudaFuncSetAttribute(bench<SPARSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench<SPARSE><<<sms, 32 * (4 + gwarps), smem>>>(src, idx, 64, do_mma, d);
-  bench<SPARSE><<<sms, 32 * (4 + gwarps), smem>>>(src, idx, iters, do_mma, d);
+  bench<SPARSE><<<sms, 32 * (4 + gwarps), smem>>>(src, idx, 64, do_mma, d, gap);
+  bench<SPARSE><<<sms, 32 * (4 + gwarps), smem>>>(src, idx, gap ? iters / 2 : iters, do_mma, d, gap);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); exit(1); }
   unsigned long long h[512];
@@ -157,8 +163,9 @@ void run(const uint4* src, const int* idx, int gwarps, int do_mma, int sms, unsi
   }
   cyc /= sms;
   rows /= sms;
-  printf("%-14s gather_warps %2d  mma %s  cycles/mma %7.1f  gather %6.1f B/clk/SM (%5.2f TB/s at 1.965 GHz)\n",
-         SPARSE ? "sparse_m64" : "dense_m128", gwarps, do_mma ? "on " : "off", do_mma ? cyc / iters : 0.0,
+  const int n_mma = gap ? iters / 2 : iters;
+  printf("%-14s gather_warps %2d  mma %s gap %5d  cycles/mma %7.1f  gather %6.1f B/clk/SM (%5.2f TB/s at 1.965 GHz)\n",
+         SPARSE ? "sparse_m64" : "dense_m128", gwarps, do_mma ? "on " : "off", gap, do_mma ? cyc / n_mma : 0.0,
          rows * 512 / cyc, rows * 512 / cyc * sms * 1.965e9 / 1e12);
 }
 
@@ -184,5 +191,7 @@ int main() {
   for (int g : {0, 8, 16, 24}) run<1>(src, idx, g, 1, sms, d);
   for (int g : {8, 16, 24}) run<1>(src, idx, g, 0, sms, d);
   for (int g : {0, 8, 16}) run<0>(src, idx, g, 1, sms, d);
+  // ~50 % MMA duty (the SpMM's tensor pipe is busy about half the time): 8 MMAs, then 2304 idle
+  for (int g : {8, 16, 24, 28}) run<1>(src, idx, g, 1, sms, d, 2304);
   return 0;
 }
