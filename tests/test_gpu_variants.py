@@ -1,0 +1,57 @@
+"""GPU: every SpMM kernel configuration the launcher can select (or an experiment switch forces)
+agrees with the CUDA-core cross-check kernel.  The switches are read once per process, so each
+configuration runs in its own subprocess: 16 setmaxnreg-rebalanced gather warps, 128-token units
+with two accumulators, programmatic dependent launch forced on / off, the M=128 instruction for
+V <= 64.  Tolerance: rtol 1e-2 / atol 1e-3 (bf16 output vs the fp32 cross-check).
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SNIPPET = r"""
+import sys
+sys.path.insert(0, {root!r})
+import torch
+import paper_2407_20496_b200 as H
+from paper_2407_20496_b200 import device as D, synth
+# shapes: LLaMA-like (many units, K > 1 stage), small K, ragged tokens, V = 32 / 128
+for V, m, n, B in ((64, 1024, 2048, 1024), (64, 256, 128, 520), (32, 256, 768, 136),
+                   (128, 512, 1024, 264), (64, 768, 768, 4096)):
+    W = torch.as_tensor(synth.randn_bf16((m, n), 5)).cuda().to(torch.bfloat16)
+    pack = H.compress(W, H.HiNMConfig(V, 2, 4, 0.5), synth.random_sigma_o(m, 6))
+    X = torch.as_tensor(synth.randn_bf16((n, B), 7)).cuda().to(torch.bfloat16)
+    for order in ("sigma", "original"):
+        Y = D.spmm(pack, X, order=order).float()
+        Yr = D.spmm_simt(pack, X, order=order)
+        torch.cuda.synchronize()
+        excess = float(((Y - Yr).abs() - (1e-3 + 1e-2 * Yr.abs())).max())
+        assert excess <= 0, (V, m, n, B, order, excess)
+print("ok")
+"""
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.mark.parametrize("env", [
+    {"HINM_GW": "16"},
+    {"HINM_BN": "128"},
+    {"HINM_PDL": "0"},
+    {"HINM_PDL": "1"},
+    {"HINM_GATHER": "m128"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_kernel_variant_matches_cross_check(env):
+    r = subprocess.run([sys.executable, "-c", SNIPPET.format(root=ROOT)], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
