@@ -323,7 +323,9 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 }
 
 // DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
-// 2 = skip the gather (measure the MMA pipeline alone).  Results are garbage when DBG != 0.
+// 2 = skip the gather (measure the MMA pipeline alone), 3 = no epilogue, 4 = no A / metadata
+// loads, 5 = gather only with every 4th row left unfetched (ring slots vs bytes).  Results are
+// garbage when DBG != 0.
 // M64: V <= 64 on the M=64 instruction (half the A-operand shared-memory reads of M=128).  Its
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         for (int k = 0; k < RPW / RPI; ++k) {
           const int i = k * RPI + rsub;  // this lane's row (of the warp's RPW)
           const uint32_t row = __shfl_sync(0xffffffffu, my_row, i);
-          if (DBG != 2 && (i * GW < 64 || full))
+          if (DBG != 2 && (i * GW < 64 || full) && !(DBG == 5 && (i & 3) == 3))
             cp_async_16(dst0 + k * RPI * GW * 128, xs + (uint64_t)row * ldx2, src_bytes);  // IMAD.WIDE.U32
         }
         cp_async_arrive_noinc(bar_full + 8 * stage);
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
           const uint32_t ecol = tmem + E_COL + eslot * 4 + (s0 & 1) * 2;
           const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
-          if (DBG != 1 && DBG != 4) {
+          if (DBG != 1 && DBG != 4 && DBG != 5) {
             mma_sp(dtm, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
             mma_sp(dtm, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
             if (two) {
@@ -812,6 +814,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_nogather")) return 3;
     if (!strcmp(e, "dbg_noepi")) return 4;
     if (!strcmp(e, "dbg_gather_x_only")) return 5;
+    if (!strcmp(e, "dbg_gather_sparse")) return 6;  // gather only, every 4th row's bytes skipped
     return 0;
   }();
   const int dev = current_device();
@@ -860,6 +863,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
   } else if (variant == 5) {
     rc = launch(k_hinm_spmm<128, 8, 4, true>, 128, 8, 256);
+  } else if (variant == 6) {
+    rc = launch(k_hinm_spmm<128, 8, 5, true>, 128, 8, 256);
   } else if (bnt == 128) {
     rc = ks == 128 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true, 128>, 128, 8, 128)
                           : launch(k_hinm_spmm<128, 8, 0, false, 128>, 128, 8, 128))
