@@ -324,7 +324,8 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 
 // DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
 // 2 = skip the gather (measure the MMA pipeline alone), 3 = no epilogue, 4 = no A / metadata
-// loads, 5 = gather only with every 4th row left unfetched (ring slots vs bytes).  Results are
+// loads, 5 = gather only with every 4th row left unfetched (ring slots vs bytes), 6 = the full
+// kernel with every 4th row unfetched (a tile-pair image's zero-filled padding).  Results are
 // garbage when DBG != 0.
 // M64: V <= 64 on the M=64 instruction (half the A-operand shared-memory reads of M=128).  Its
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         for (int k = 0; k < RPW / RPI; ++k) {
           const int i = k * RPI + rsub;  // this lane's row (of the warp's RPW)
           const uint32_t row = __shfl_sync(0xffffffffu, my_row, i);
-          if (DBG != 2 && (i * GW < 64 || full) && !(DBG == 5 && (i & 3) == 3))
+          if (DBG != 2 && (i * GW < 64 || full) && !((DBG == 5 || DBG == 6) && (i & 3) == 3))
             cp_async_16(dst0 + k * RPI * GW * 128, xs + (uint64_t)row * ldx2, src_bytes);  // IMAD.WIDE.U32
         }
         cp_async_arrive_noinc(bar_full + 8 * stage);
@@ -815,6 +816,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_noepi")) return 4;
     if (!strcmp(e, "dbg_gather_x_only")) return 5;
     if (!strcmp(e, "dbg_gather_sparse")) return 6;  // gather only, every 4th row's bytes skipped
+    if (!strcmp(e, "dbg_pad_quarter")) return 7;    // full kernel, every 4th row unfetched (padding)
     return 0;
   }();
   const int dev = current_device();
@@ -863,6 +865,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
   } else if (variant == 5) {
     rc = launch(k_hinm_spmm<128, 8, 4, true>, 128, 8, 256);
+  } else if (variant == 7) {
+    rc = m64 ? launch(k_hinm_spmm<128, 8, 6, true>, 128, 8, 256) : launch(k_hinm_spmm<64, 8, 6, false>, 64, 8, 256);
   } else if (variant == 6) {
     rc = launch(k_hinm_spmm<128, 8, 5, true>, 128, 8, 256);
   } else if (bnt == 128) {
