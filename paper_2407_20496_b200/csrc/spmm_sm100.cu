@@ -325,7 +325,8 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // DBG (experiments only): 1 = skip the MMAs (measure the gather pipeline alone),
 // 2 = skip the gather (measure the MMA pipeline alone), 3 = no epilogue, 4 = no A / metadata
 // loads, 5 = gather only with every 4th row left unfetched (ring slots vs bytes), 6 = the full
-// kernel with every 4th row unfetched (a tile-pair image's zero-filled padding).  Results are
+// kernel with every 4th row unfetched (a tile-pair image's zero-filled padding), 7 = the full kernel
+// loading the A image on even token blocks only (A shared by two token blocks).  Results are
 // garbage when DBG != 0.
 // M64: V <= 64 on the M=64 instruction (half the A-operand shared-memory reads of M=128).  Its
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
@@ -420,7 +421,8 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
       for (int s = 0; s < nst; s += KS / BK) {             // one A stage per X stage
         mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
         const uint32_t fb = bar_afull + 8 * aslot;
-        if (DBG == 4) {  // experiment: no A / metadata loads at all
+        if (DBG == 4 || (DBG == 7 && (cur.nb & 1))) {  // experiments: no A / metadata loads
+          // (DBG 7: on every other token block, i.e. the A image read once per 512 tokens)
           if (elect_one()) mbar_arrive(fb);
         } else if (elect_one()) {
           const uint32_t a_bytes = V * 64 * min(KS / BK, nst - s);
@@ -817,6 +819,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     if (!strcmp(e, "dbg_gather_x_only")) return 5;
     if (!strcmp(e, "dbg_gather_sparse")) return 6;  // gather only, every 4th row's bytes skipped
     if (!strcmp(e, "dbg_pad_quarter")) return 7;    // full kernel, every 4th row unfetched (padding)
+    if (!strcmp(e, "dbg_half_a")) return 8;         // full kernel, A image loaded for even token blocks only
     return 0;
   }();
   const int dev = current_device();
@@ -865,6 +868,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
   } else if (variant == 5) {
     rc = launch(k_hinm_spmm<128, 8, 4, true>, 128, 8, 256);
+  } else if (variant == 8) {
+    rc = launch(k_hinm_spmm<128, 8, 7, true>, 128, 8, 256);
   } else if (variant == 7) {
     rc = m64 ? launch(k_hinm_spmm<128, 8, 6, true>, 128, 8, 256) : launch(k_hinm_spmm<64, 8, 6, false>, 64, 8, 256);
   } else if (variant == 6) {
