@@ -803,9 +803,10 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   // small-K shapes included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @ 802816
   // 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is re-read
   // twice as often.  It is used only when the units would otherwise leave SMs idle.
-  // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_GATHER = m128
-  // (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi | dbg_gather_x_only
-  // (timing only: results are garbage).
+  // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_PDL = 0 | 1,
+  // HINM_GATHER = m128 (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi |
+  // dbg_gather_x_only | dbg_gather_sparse | dbg_pad_quarter | dbg_half_a (timing only: results are
+  // garbage; see the DBG note above the kernel).
   static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
   static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
   static const int env_bn = getenv("HINM_BN") ? atoi(getenv("HINM_BN")) : 0;
@@ -868,12 +869,12 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = launch(k_hinm_spmm<128, 8, 3, true>, 128, 8, 256);
   } else if (variant == 5) {
     rc = launch(k_hinm_spmm<128, 8, 4, true>, 128, 8, 256);
-  } else if (variant == 8) {
-    rc = launch(k_hinm_spmm<128, 8, 7, true>, 128, 8, 256);
-  } else if (variant == 7) {
-    rc = m64 ? launch(k_hinm_spmm<128, 8, 6, true>, 128, 8, 256) : launch(k_hinm_spmm<64, 8, 6, false>, 64, 8, 256);
   } else if (variant == 6) {
     rc = launch(k_hinm_spmm<128, 8, 5, true>, 128, 8, 256);
+  } else if (variant == 7) {
+    rc = m64 ? launch(k_hinm_spmm<128, 8, 6, true>, 128, 8, 256) : launch(k_hinm_spmm<64, 8, 6, false>, 64, 8, 256);
+  } else if (variant == 8) {
+    rc = launch(k_hinm_spmm<128, 8, 7, true>, 128, 8, 256);
   } else if (bnt == 128) {
     rc = ks == 128 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true, 128>, 128, 8, 128)
                           : launch(k_hinm_spmm<128, 8, 0, false, 128>, 128, 8, 128))
