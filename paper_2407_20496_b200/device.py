@@ -28,8 +28,10 @@ def _stream_handle(device=None) -> int:
     torch = _torch()
     raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
     if raw is not None:  # ~10x cheaper than current_stream() on the per-call launch path
-        idx = device.index if hasattr(device, "index") else device
-        return raw(torch.cuda.current_device() if idx is None else idx)
+        if isinstance(device, str):
+            device = torch.device(device)
+        idx = device.index if isinstance(device, torch.device) else device
+        return raw(torch.cuda.current_device() if idx is None else int(idx))
     return torch.cuda.current_stream(device).cuda_stream
 
 
