@@ -322,7 +322,11 @@ def run_ours(args):
                                  "achieved_tbs": round(l2_tbs, 2), "cap_tbs": 21.2,
                                  "frac": round(l2_tbs / 21.2, 3),
                                  "cap_source": "scripts/l2_ring.cu on B200: 16 warps x 128-row stages, "
-                                               "no MMA (profiles/r01_gather_microbench.txt)"}},
+                                               "no MMA (profiles/r01_gather_microbench.txt)",
+                                 # the L2->SMEM ceiling of free-running cp.async (24-32 issuing
+                                 # warps, no ring, no MMA; profiles/r01_gather_contention.txt)
+                                 "cap_tbs_free_running": 27.0,
+                                 "frac_free_running": round(l2_tbs / 27.0, 3)}},
         "compressor": {"ms": {k: round(v, 3) for k, v in comp_ms.items()},
                        "stream_ms": {k: round(v, 3) for k, v in comp_gpu_ms.items()},
                        "algorithmic_bytes": comp_bytes,
