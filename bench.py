@@ -1,20 +1,25 @@
 """Benchmark: HiNM SpMM effective TFLOPS and speed-up vs cuBLAS dense bf16 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[2], the headline target): one LLaMA-7B FFN layer at 75% HiNM
-sparsity (V=64, 2:4, s_v=0.5) on 16384 tokens -- gate + up (11008x4096) and down
+Default workload (BASELINE.json configs[2], the headline target): one LLaMA-7B FFN layer at 75%
+HiNM sparsity (V=64, 2:4, s_v=0.5) on 16384 tokens -- gate + up (11008x4096) and down
 (4096x11008) SpMMs per step, the down projection consuming the up projection's output in
 original channel order (the sigma_o restore is fused in the epilogue).  Token-sharded over N
-GPUs with replicated packed weights and no collective in the timed region.  Weak scaling by
-default (the path partitions into independent token shards): every rank runs the 16384-token
-workload on its own shard, so N ranks process N x 16384 tokens; --strong keeps 16384 global
-tokens split N ways.  Synthetic N(0,1) bf16 weights/activations, seeded; random sigma_o.
+GPUs (one process per GPU): rank 0 compresses the weights and replicates the packs over NCCL
+(shard.broadcast_pack, outside the timed region), every rank runs its contiguous token slice
+(shard.shard_bounds) with no collective in the timed region.  Strong scaling by default
+(16384 global tokens -> 2048 per GPU at N=8, BASELINE cfg3); --weak keeps 16384 per GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+                    [--config llama|cfg1|cfg2|cfg4|cfg5] [--weak] [--tokens T]
 
-The reference arm (--impl reference) times the CPU oracle port of the reference's hinm_spmm
-(oracle/hinm_oracle.py, gather + per-row GEMV in float64, all host BLAS threads) on a bounded
-sample of the same workload; rank 0 only.
+With --gpus N > 1 and no WORLD_SIZE in the environment the script re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal
+--gpus.  --dry-run exercises that plumbing on CPU (gloo, no kernels) for the tests.
+
+The reference arm (--impl reference) times the reference's own CPU implementation
+(oracle/_ref = the unmodified `hinm` package installed by oracle/install_ref.sh; the numpy
+oracle port when it is absent) on the box's host cores, on a bounded token sample of the same
+workload; rank 0 only.
 """
 
 from __future__ import annotations
@@ -22,6 +27,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,6 +42,7 @@ M_FFN, N_FFN = 11008, 4096
 V, NM_N, NM_M, SV = 64, 2, 4, 0.5
 GLOBAL_TOKENS = 16384
 METRIC = "HiNM SpMM effective TFLOPS (LLaMA-7B FFN gate+up+down, 75% HiNM V=64 2:4)"
+L2_BYTES = 126 * 2 ** 20
 
 
 def peaks():
@@ -54,14 +61,32 @@ def eff_flops(tokens):
     return sum(2.0 * m * n * tokens for _, m, n in layer_shapes())
 
 
-def sparse_flops(tokens):
-    return sum(2.0 * m * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
+def sparse_flops(tokens, sv=SV):
+    return sum(2.0 * m * int(n * (1 - sv)) * tokens for _, m, n in layer_shapes())
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:  # pragma: no cover
+        return os.cpu_count()
+
+
+def all_host_threads():
+    """The CPU arms use every host core: torchrun sets OMP_NUM_THREADS=1 per rank, so the BLAS
+    pools are widened explicitly (threadpoolctl)."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:  # pragma: no cover
+        return None
 
 
 class ClockSampler:
     """SM clock and throttle reasons sampled through NVML every 5 ms while the timed region runs
-    (a background thread; nvidia-smi's 100 ms floor is longer than the timed region).  Falls back
-    to nvidia-smi when NVML is unavailable."""
+    (a background thread; nvidia-smi's 100 ms floor is longer than the timed region)."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -119,158 +144,290 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-def run_ours(args):
+# process plumbing
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: re-launch this script with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+class Dist:
+    """World / rank of this process (torchrun env) and the max-over-ranks reduction."""
+
+    def __init__(self, backend: str, device=None):
+        import torch.distributed as dist
+
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = dist
+        if self.world > 1:
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=device)
+            else:
+                dist.init_process_group("gloo")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, value: float, device=None) -> float:
+        if self.world == 1:
+            return value
+        import torch
+
+        t = torch.tensor([value], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def token_shard(args, d: Dist):
+    """(global tokens, [lo, hi) of this rank): strong scaling splits args.tokens over the ranks."""
+    from paper_2407_20496_b200.shard import shard_bounds
+
+    if args.weak:
+        return args.tokens * d.world, (0, args.tokens)
+    return args.tokens, shard_bounds(args.tokens, d.world, d.rank)
+
+
+def run_dry(args):
+    """CPU plumbing check (gloo, no kernels): world, shards, pack replication, max over ranks."""
+    d = Dist("gloo")
+    global_tokens, (lo, hi) = token_shard(args, d)
+    meta = [{"layers": [list(s) for s in layer_shapes()]} if d.rank == 0 else None]
+    if d.world > 1:
+        d.dist.broadcast_object_list(meta, src=0)
+    ms = d.max(float(d.rank + 1))
+    if d.rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": d.world, "global_tokens": global_tokens,
+                          "tokens_rank0": hi - lo, "layers": meta[0]["layers"],
+                          "max_over_ranks": ms, "scaling": "weak" if args.weak else "strong"}),
+              flush=True)
+    d.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# timing helpers
+def _events(torch, k):
+    return [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+
+
+def l2_flush_buffer(torch, dev):
+    return torch.empty(512 * 2 ** 20 // 4, dtype=torch.int32, device=dev)
+
+
+def gather_ceiling():
+    """The L2->SMEM fill ceiling of the gather on THIS box (scripts/gather_mechanisms --ceiling:
+    cp.async 16 B/lane from a 32 KB-pitched X, with and without the M=64 sparse MMA stream)."""
+    exe = os.path.join(ROOT, "scripts", "bin", "gather_mechanisms")
+    if not os.path.exists(exe):
+        return None
+    try:
+        r = subprocess.run([exe, "--ceiling"], capture_output=True, text=True, timeout=120)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception:  # pragma: no cover - measurement tool failure is reported, not fatal
+        return None
+
+
+# ------------------------------------------------------------------------------------------------
+def run_llama(args):
     import torch
-    import torch.distributed as dist
 
     import paper_2407_20496_b200 as H
     from paper_2407_20496_b200 import _lib
     from paper_2407_20496_b200.build import build as _build
+    from paper_2407_20496_b200.shard import broadcast_pack
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if rank == 0:
+    d = Dist("nccl", dev)
+    if d.rank == 0:
         _build(force=False, verbose=False)
-    if world > 1:
-        dist.barrier()
+    d.barrier()
     lib = _lib.load()
+    global_tokens, (lo, hi) = token_shard(args, d)
+    tokens = hi - lo
+    cfg = H.HiNMConfig(args.v, NM_N, NM_M, SV)
 
-    # token shard of this rank: weak scaling (default) keeps 16384 tokens per rank
-    global_tokens = GLOBAL_TOKENS if args.strong else GLOBAL_TOKENS * world
-    tokens = global_tokens // world
-    cfg = H.HiNMConfig(V, NM_N, NM_M, SV)
-    g = torch.Generator(device=dev)
-    packs, dense = {}, {}
-    comp_ms, comp_gpu_ms = {}, {}
+    # weights: rank 0 compresses, NCCL replicates the packs (outside the timed region)
+    packs, dense, comp = {}, {}, {}
     for i, (name, m, n) in enumerate(layer_shapes()):
-        g.manual_seed(1000 + i)                          # same weights on every rank (replicated)
+        g = torch.Generator(device=dev).manual_seed(1000 + i)
         W = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-        so = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
-        H.compress(W, cfg, so)                           # warm-up (allocator, cub, attributes)
-        torch.cuda.synchronize()
-        ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        ce0.record()
-        packs[name] = H.compress(W, cfg, so)
-        ce1.record()
-        torch.cuda.synchronize()
-        comp_ms[name] = (time.perf_counter() - t0) * 1e3
-        comp_gpu_ms[name] = ce0.elapsed_time(ce1)
         dense[name] = W
-    g.manual_seed(7 + rank)
-    X = torch.randn(N_FFN, tokens, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    y_gate = torch.empty(M_FFN, tokens, dtype=torch.bfloat16, device=dev)
-    y_up = torch.empty(M_FFN, tokens, dtype=torch.bfloat16, device=dev)
-    y_down = torch.empty(N_FFN, tokens, dtype=torch.bfloat16, device=dev)
-
+        so = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
+        if d.rank == 0:
+            H.compress(W, cfg, so)                       # warm-up (allocator, cub, attributes)
+            torch.cuda.synchronize()
+            ce0, ce1 = _events(torch, 2)
+            t0 = time.perf_counter()
+            ce0.record()
+            packs[name] = H.compress(W, cfg, so)
+            ce1.record()
+            torch.cuda.synchronize()
+            comp[name] = ((time.perf_counter() - t0) * 1e3, ce0.elapsed_time(ce1))
+        if d.world > 1:
+            packs[name] = broadcast_pack(packs.get(name), src=0, device=dev)
+    torch.cuda.synchronize()
+    gx = torch.Generator(device=dev).manual_seed(7)
+    X_full = torch.randn(N_FFN, args.tokens if not args.weak else tokens, generator=gx, device=dev,
+                         dtype=torch.float32).to(torch.bfloat16)
+    X = X_full[:, lo:hi].contiguous() if not args.weak else X_full
+    del X_full
+    y = {nm: torch.empty(m, tokens, dtype=torch.bfloat16, device=dev) for nm, m, _ in layer_shapes()}
     names = [nm for nm, _, _ in layer_shapes()]
-    ev = None  # per-launch CUDA events inside the timed region (roofline: per-kernel durations)
 
-    def step(x, i=None):
-        evs = ev[i] if ev is not None and i is not None else None
+    def step(evs=None):
         if evs: evs[0].record()
-        H.spmm(packs["gate"], x, out=y_gate, order="original")
+        H.spmm(packs["gate"], X, out=y["gate"], order="original")
         if evs: evs[1].record()
-        H.spmm(packs["up"], x, out=y_up, order="original")
+        H.spmm(packs["up"], X, out=y["up"], order="original")
         if evs: evs[2].record()
-        H.spmm(packs["down"], y_up, out=y_down, order="original")
+        H.spmm(packs["down"], y["up"], out=y["down"], order="original")
         if evs: evs[3].record()
-        return y_down
 
-    def timed(fn, iters):
-        if world > 1:
-            dist.barrier()
+    def timed(fn, iters, per_iter_events=0):
+        """barrier + synchronize on both sides, CUDA events on the launching stream, max over ranks"""
+        evs = [_events(torch, per_iter_events) for _ in range(iters)] if per_iter_events else None
+        d.barrier()
         torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s, e = _events(torch, 2)
         s.record()
-        for _ in range(iters):
-            fn()
+        for i in range(iters):
+            fn(evs[i] if evs else None)
         e.record()
         torch.cuda.synchronize()
-        ms = s.elapsed_time(e)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        ms = d.max(s.elapsed_time(e), dev)
+        return ms, evs
 
     for _ in range(args.warmup):
-        step(X)
-    torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    it = iter(range(args.steps))
+        step()
     with ClockSampler(local) as clk:
-        ms_total = timed(lambda: step(X, next(it)), args.steps)
-    per_kernel = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in ev) / args.steps for j, nm in enumerate(names)}
-    step_ms = sorted(e[0].elapsed_time(e[3]) for e in ev)
+        ms_total, evs = timed(step, args.steps, 4)
+    per_kernel = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in evs) / args.steps
+                  for j, nm in enumerate(names)}
+    step_ms = sorted(e[0].elapsed_time(e[3]) for e in evs)
     pct = lambda q: step_ms[min(len(step_ms) - 1, int(q * (len(step_ms) - 1) + 0.5))]  # noqa: E731
-    ev = None
     launches = 3 * args.steps                            # hinm_spmm_bf16 launches one kernel each
     assert lib.hinm_last_launch_count() == 1
     ms_step = ms_total / args.steps
     value = eff_flops(global_tokens) / (ms_step * 1e-3) / 1e12
 
-    # cuBLAS dense comparator on the same shapes, measured the same way as our step (W warm-up
-    # steps, K timed steps of the three GEMMs back to back, per-GEMM events) after a 1 s pause:
+    # L2-cold step: a 512 MB write between steps evicts L2; only the step itself is timed
+    flush = l2_flush_buffer(torch, dev)
+    cold = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(1)
+        s, e = _events(torch, 2)
+        s.record()
+        step()
+        e.record()
+        torch.cuda.synchronize()
+        cold.append(s.elapsed_time(e))
+    ms_cold = d.max(statistics.median(cold), dev)
+    del flush
+
+    # cuBLAS dense comparator on the same shapes and shard, same protocol, after a 1 s pause:
     # sustained load engages the 1 kW power cap within ~0.1 s (SM clock 1965 -> ~1700 MHz,
     # scripts/sustained_check.py), so both arms are timed from the same uncapped state
-    gemm_out = {nm: torch.empty(m, tokens, dtype=torch.bfloat16, device=dev)
-                for nm, m, _ in layer_shapes()}
+    gout = {nm: torch.empty(m, tokens, dtype=torch.bfloat16, device=dev) for nm, m, _ in layer_shapes()}
 
-    def dense_step(i=None):
-        evs = ev[i] if ev is not None and i is not None else None
+    def dense_step(evs=None):
         for j, (nm, _, _) in enumerate(layer_shapes()):
             if evs: evs[j].record()
-            torch.matmul(dense[nm], X if nm != "down" else gemm_out["up"], out=gemm_out[nm])
+            torch.matmul(dense[nm], X if nm != "down" else gout["up"], out=gout[nm])
         if evs: evs[3].record()
 
     torch.cuda.synchronize()
     time.sleep(1.0)
     for _ in range(args.warmup):
         dense_step()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    it = iter(range(args.steps))
     with ClockSampler(local) as clk_cublas:
-        timed(lambda: dense_step(next(it)), args.steps)
-    cublas = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in ev) / args.steps for j, nm in enumerate(names)}
-    ev = None
-    ms_cublas_step = sum(cublas.values())
+        ms_cublas_total, cev = timed(dense_step, args.steps, 4)
+    cublas = {nm: sum(e[j].elapsed_time(e[j + 1]) for e in cev) / args.steps for j, nm in enumerate(names)}
+    ms_cublas_step = ms_cublas_total / args.steps
     cublas_tflops = eff_flops(global_tokens) / (ms_cublas_step * 1e-3) / 1e12
 
-    # end to end through the public API (HostChain -> hinm_chain_run_host): pinned host X in,
+    # end to end through the public API (HostChain -> hinm_chain_run_host): pinned host X shard in,
     # Y_down out, every step; H2D / SpMMs / D2H of consecutive token chunks overlap
     xh = X.cpu().pin_memory()
     yh = torch.empty(N_FFN, tokens, dtype=torch.bfloat16).pin_memory()
-    chunk = max(512, (tokens // 8) // 256 * 256)
+    chunk = max(256, min(2048, (tokens // 8) // 256 * 256))
     chain = H.HostChain([(packs["gate"], 0, 1, "original"), (packs["up"], 0, 2, "original"),
                          (packs["down"], 2, 3, "original")], out_buf=3, chunk=chunk, device=dev)
-
-    def e2e_step():
-        chain.run(xh, yh)
-
     for _ in range(max(1, args.warmup // 2)):
-        e2e_step()
-    ms_e2e = timed(e2e_step, args.steps) / args.steps
+        chain.run(xh, yh)
+    ms_e2e = timed(lambda _e: chain.run(xh, yh), args.steps)[0] / args.steps
+    # the host link itself: one pinned H2D + D2H of the same bytes with plain cudaMemcpy
+    xd = torch.empty_like(X)
+    s, e = _events(torch, 2)
+    s.record()
+    xd.copy_(xh, non_blocking=True)
+    yh.copy_(y["down"], non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    ms_link = s.elapsed_time(e)
 
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+    result = None
+    if d.rank == 0:
+        result = llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value,
+                            ms_cold, cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e,
+                            ms_link, xh, yh, chunk, launches)
+    # secondary rows (rank 0, N=1 only): the same step at V=128
+    if d.world == 1 and not args.no_extras and args.v == 64:
+        result["v128"] = v128_row(H, torch, dev, X, y, args, cublas, global_tokens)
+    if d.rank == 0:
+        if d.world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(packs, args.cpu_tokens)
+        print(json.dumps(result), flush=True)
+    d.close()
+
+
+def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value, ms_cold,
+               cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e, ms_link, xh, yh, chunk,
+               launches):
     pk, kind = peaks()
     p_sparse = 2.0 * pk["bf16_tflops"]
     f_sp = sparse_flops(tokens)
     achieved = f_sp / (sum(per_kernel.values()) * 1e-3) / 1e12
-    # the gather roofline: every kept K-row of a tile is streamed L2 -> SMEM once per 256-token
-    # block (2 * T * k_bar * tokens bytes) plus the compressed A / metadata image per unit
-    gathered = sum(2.0 * (m // V) * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
-    a_image = sum((m // V) * int(n * (1 - SV)) * V * 1.125 * -(-tokens // 256) for _, m, n in layer_shapes())
+    # dominant kernel: the gate / up projection (11008 x 4096), per launch
+    f_up = 2.0 * M_FFN * int(N_FFN * (1 - SV)) * tokens
+    ach_up = f_up / (per_kernel["up"] * 1e-3) / 1e12
+    # the gather: every kept K-row of a tile is streamed L2 -> SMEM once per 256-token block
+    # (2 * T * k_bar * tokens bytes) plus the compressed A / metadata image per unit
+    gathered = sum(2.0 * (m // args.v) * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
+    a_image = sum((m // args.v) * int(n * (1 - SV)) * args.v * 1.125 * -(-tokens // 256)
+                  for _, m, n in layer_shapes())
+    l2_bclk = None
     l2_tbs = (gathered + a_image) / (sum(per_kernel.values()) * 1e-3) / 1e12
+    ceiling = gather_ceiling()
+    binding = {"resource": "L2->SMEM gather fill (cp.async, 16 B per lane)",
+               "achieved_tbs": round(l2_tbs, 2)}
+    sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+    l2_bclk = l2_tbs * 1e12 / (148 * sm_mhz * 1e6)
+    binding["achieved_bclk_per_sm"] = round(l2_bclk, 1)
+    if ceiling:
+        cap = ceiling["fill_under_mma_bclk_sm"]
+        binding.update({"cap_bclk_per_sm_under_mma": cap, "cap_bclk_per_sm_alone": ceiling["fill_alone_bclk_sm"],
+                        "frac": round(l2_bclk / cap, 3),
+                        "cap_source": "measured in this run: scripts/bin/gather_mechanisms --ceiling ("
+                                      + ceiling["mechanism"] + ")"})
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "spmm_dram_traffic.json")))
@@ -280,131 +437,255 @@ def run_ours(args):
     comp_bytes = 0
     for name, m, n in layer_shapes():
         kbar = int(n * (1 - SV))
-        comp_bytes += 2 * m * n + m * kbar + m * kbar // 8 + 4 * (m // V) * kbar + 4 * m
-    result = {
+        comp_bytes += 2 * m * n + m * kbar + m * kbar // 8 + 4 * (m // args.v) * kbar + 4 * m
+    comp_ms = sum(c[0] for c in comp.values())
+    comp_gpu = sum(c[1] for c in comp.values())
+    strong = not args.weak
+    return {
         "metric": METRIC,
         "value": round(value, 2),
         "unit": "TFLOP/s",
-        "n_gpus": world,
+        "n_gpus": d.world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "ms_per_step_p10_p50_p90": [round(pct(0.1), 4), round(pct(0.5), 4), round(pct(0.9), 4)],
         "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 weights/activations, random sigma_o)",
         "config": {
-            "workload": "LLaMA-7B FFN layer (gate+up 11008x4096, down 4096x11008), 75% HiNM "
-                        "V=64 2:4 s_v=0.5, " + ("16384 tokens token-sharded" if args.strong else
-                                                "16384 tokens per GPU, token-sharded"),
+            "workload": f"LLaMA-7B FFN layer (gate+up 11008x4096, down 4096x11008), 75% HiNM V={args.v} "
+                        f"2:4 s_v=0.5, {global_tokens} tokens" + (" token-sharded" if strong else
+                                                                  " per GPU x N"),
             "global_tokens": global_tokens, "tokens_per_gpu": tokens,
-            "parallelism": f"token-shard x{world}, weights replicated, no collective",
-            "l2": "inputs larger than L2 (X 134 MB + 3 packs ~150 MB per step at N=1)",
+            "parallelism": f"token-shard x{d.world} (shard.shard_bounds), packs replicated from rank 0 "
+                           "(shard.broadcast_pack), no collective in the timed region",
+            "l2": "inputs larger than L2 (per step: X + 3 packs + 3 outputs "
+                  f"~{(2 * N_FFN * tokens + 2 * (2 * M_FFN + N_FFN) * tokens + 3 * 25e6) / 1e6:.0f} MB "
+                  "per GPU); l2_cold_ms_per_step flushes L2 with a 512 MB write between steps",
         },
         "speedup_vs_cublas": round(ms_cublas_step / ms_step, 3),
+        "l2_cold_ms_per_step": round(ms_cold, 4),
         "cublas_dense_bf16": {"tflops": round(cublas_tflops, 2), "ms_per_step": round(ms_cublas_step, 4),
                               "per_gemm_ms": {k: round(v, 4) for k, v in cublas.items()},
                               "clocks": clk_cublas.summary(),
                               "protocol": "same W/K step protocol as value, after a 1 s pause"},
         "per_spmm_ms": {k: round(v, 4) for k, v in per_kernel.items()},
-        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(p_sparse, 1),
-                     "unit": "TFLOP/s", "frac": round(achieved / p_sparse, 4), "traffic": traffic,
+        "roofline": {"bound": "tensor", "achieved": round(ach_up, 1), "peak": round(p_sparse, 1),
+                     "unit": "TFLOP/s", "frac": round(ach_up / p_sparse, 4), "traffic": traffic,
+                     "kernel": "k_hinm_spmm, up projection 11008x4096 (the dominant launch)",
+                     "achieved_step_all_spmms": round(achieved, 1),
+                     "frac_step_all_spmms": round(achieved / p_sparse, 4),
                      "peak_source": f"2 x bf16_tflops of {kind} MEASURED_PEAKS.json (2:4 sparse)",
                      "algorithmic": "2*m*k_bar*tokens per SpMM (k_bar = n/2 kept vectors)",
                      "traffic_note": (tr or {}).get("note"),
                      # the V=64 tile runs on the M=64 sparse instruction: 144 cycles per
-                     # 64x256x32 MMA = 1964 TF/s logical on 148 SMs (scripts/mma_rate.cu)
+                     # 64x256x32 MMA = 1964 TF/s on 148 SMs at 1.965 GHz (scripts/mma_rate.cu)
                      "instruction_ceiling": 1964.4,
-                     "frac_of_instruction_ceiling": round(achieved / 1964.4, 4),
-                     "binding": {"resource": "L2->SMEM gather (cp.async)",
-                                 "achieved_tbs": round(l2_tbs, 2), "cap_tbs": 21.2,
-                                 "frac": round(l2_tbs / 21.2, 3),
-                                 "cap_source": "scripts/l2_ring.cu on B200: 16 warps x 128-row stages, "
-                                               "no MMA (profiles/r01_gather_microbench.txt)",
-                                 # the L2->SMEM ceiling of free-running cp.async (24-32 issuing
-                                 # warps, no ring, no MMA; profiles/r01_gather_contention.txt)
-                                 "cap_tbs_free_running": 27.0,
-                                 "frac_free_running": round(l2_tbs / 27.0, 3)}},
-        "compressor": {"ms": {k: round(v, 3) for k, v in comp_ms.items()},
-                       "stream_ms": {k: round(v, 3) for k, v in comp_gpu_ms.items()},
+                     "frac_of_instruction_ceiling": round(ach_up / 1964.4, 4),
+                     "binding": binding},
+        "compressor": {"ms": {k: round(v[0], 3) for k, v in comp.items()},
+                       "stream_ms": {k: round(v[1], 3) for k, v in comp.items()},
                        "algorithmic_bytes": comp_bytes,
-                       "gbs": round(comp_bytes / (sum(comp_ms.values()) * 1e-3) / 1e9, 1),
-                       "gbs_stream": round(comp_bytes / (sum(comp_gpu_ms.values()) * 1e-3) / 1e9, 1),
-                       "hbm_frac_stream": round(comp_bytes / (sum(comp_gpu_ms.values()) * 1e-3) / 1e9
-                                                / pk["hbm_gbs"], 4),
-                       "note": "ms: host wall per layer incl. allocation + sigma validation sync; "
-                               "stream_ms: CUDA events around the call; 3 layers"},
+                       "gbs": round(comp_bytes / (comp_ms * 1e-3) / 1e9, 1),
+                       "gbs_stream": round(comp_bytes / (comp_gpu * 1e-3) / 1e9, 1),
+                       "hbm_frac_stream": round(comp_bytes / (comp_gpu * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                       "note": "ms: host wall per layer; stream_ms: CUDA events around the call; 3 layers, "
+                               "rank 0"},
         "e2e": {"value": round(eff_flops(global_tokens) / (ms_e2e * 1e-3) / 1e12, 2),
                 "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2),
-                "path": f"HostChain (hinm_chain_run_host), {chunk}-token chunks, pinned host buffers"},
+                "path": f"HostChain (hinm_chain_run_host), {chunk}-token chunks, pinned host buffers",
+                "host_link_ms": round(ms_link, 4),
+                "host_link_note": "one plain pinned H2D of X + D2H of Y (cudaMemcpy, same bytes, rank 0)"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(packs["down"], args.cpu_tokens)
-    print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
-def cpu_baseline(pack, tokens: int, min_seconds: float = 10.0):
-    """Oracle port of hinm_spmm (float64 gather + GEMV, host BLAS) on a bounded token sample,
-    repeated until about min_seconds of CPU work have been timed."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import hinm_oracle as O
+def v128_row(H, torch, dev, X, y, args, cublas, global_tokens):
+    """The same LLaMA step at V=128 (2:4, s_v=0.5): secondary measured row."""
+    cfg = H.HiNMConfig(128, NM_N, NM_M, SV)
+    packs = {}
+    for i, (name, m, n) in enumerate(layer_shapes()):
+        g = torch.Generator(device=dev).manual_seed(1000 + i)
+        W = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        so = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
+        packs[name] = H.compress(W, cfg, so)
 
+    def step():
+        H.spmm(packs["gate"], X, out=y["gate"], order="original")
+        H.spmm(packs["up"], X, out=y["up"], order="original")
+        H.spmm(packs["down"], y["up"], out=y["down"], order="original")
+
+    torch.cuda.synchronize()
+    time.sleep(1.0)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    s, e = _events(torch, 2)
+    s.record()
+    for _ in range(args.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    cb = sum(cublas.values())
+    pk, _ = peaks()
+    ach = sparse_flops(X.shape[1]) / (ms * 1e-3) / 1e12
+    return {"V": 128, "ms_per_step": round(ms, 4), "value": round(eff_flops(global_tokens) / (ms * 1e-3) / 1e12, 2),
+            "speedup_vs_cublas": round(cb / ms, 3),
+            "frac_sparse_peak": round(ach / (2.0 * pk["bf16_tflops"]), 4)}
+
+
+# ------------------------------------------------------------------------------------------------
+def _reference_module():
+    """The unmodified reference package from oracle/_ref (oracle/install_ref.sh), or None."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "hinm")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
     try:
-        from threadpoolctl import threadpool_info
-        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        import hinm
+        return hinm
     except Exception:  # pragma: no cover
-        blas_threads = os.cpu_count()
-    tiles = pack.to_host_tiles()
+        return None
+
+
+def _ref_encoding(hinm, pack):
+    """Our (bit-exact) compressed layer as the reference's own HiNMEncoding type."""
+    cfg = hinm.HiNMConfig(vector_size=pack.V, nm_keep=pack.N, nm_group=pack.M,
+                          vector_sparsity=pack.config.vector_sparsity)
+    tiles = tuple(hinm.TileEncoding(vi, nm, kv) for vi, nm, kv in pack.to_host_tiles())
+    return hinm.HiNMEncoding(shape=(pack.m, pack.n), config=cfg,
+                             sigma_o=pack.sigma_o.cpu().numpy().astype(np.int64), tiles=tiles)
+
+
+def cpu_baseline(packs, tokens: int, min_seconds: float = 10.0):
+    """The reference's own hinm_spmm + restore_row_order (oracle/_ref) on the three layers of the
+    step (identical encodings), on a bounded token sample, repeated for ~min_seconds; falls back
+    to the oracle port when the reference package is absent.  Also cfg1 (BASELINE configs[0])
+    at its own shape through the reference's full CPU path."""
+    hinm = _reference_module()
+    _pool = all_host_threads()  # noqa: F841  (kept alive for the measurement)
     rng = np.random.default_rng(1)
-    X = rng.standard_normal((pack.n, tokens)).astype(np.float32).astype(np.float64)
-    so = pack.sigma_o.cpu().numpy()
+    X = rng.standard_normal((N_FFN, tokens)).astype(np.float32).astype(np.float64)
+    if hinm is not None:
+        from hinm.pruning import restore_row_order
+        encs = {k: _ref_encoding(hinm, p) for k, p in packs.items()}
+
+        def one():
+            restore_row_order(hinm.hinm_spmm(encs["gate"], X), encs["gate"].sigma_o)
+            up = restore_row_order(hinm.hinm_spmm(encs["up"], X), encs["up"].sigma_o)
+            restore_row_order(hinm.hinm_spmm(encs["down"], up), encs["down"].sigma_o)
+        kind, what = "reference", "oracle/_ref hinm.hinm_spmm + restore_row_order (unmodified reference)"
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import hinm_oracle as O
+        tl = {k: (p.to_host_tiles(), p.sigma_o.cpu().numpy()) for k, p in packs.items()}
+
+        def one():
+            for k, xin in (("gate", X), ("up", X)):
+                t, so = tl[k]
+                yk = O.restore_row_order(O.hinm_spmm(t, xin, M_FFN, V, NM_N, NM_M), so)
+            t, so = tl["down"]
+            O.restore_row_order(O.hinm_spmm(t, yk, N_FFN, V, NM_N, NM_M), so)
+        kind, what = "port", "oracle/hinm_oracle.py hinm_spmm + restore_row_order (numpy port)"
     reps, t0 = 0, time.perf_counter()
     while True:
-        Y = O.hinm_spmm(tiles, X, pack.m, pack.V, pack.N, pack.M)
-        O.restore_row_order(Y, so)
+        one()
         reps += 1
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
             break
-    f = 2.0 * pack.m * pack.n * tokens * reps
-    return {"value": round(f / dt / 1e12, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
-            "kind": "port", "seconds": round(dt, 2),
-            "sample": f"down projection 4096x11008 (V=64 2:4), {reps} x {tokens} tokens, oracle "
-                      f"hinm_spmm + restore_row_order, float64; host cpu_count={os.cpu_count()}"}
+    out = {"value": round(eff_flops(tokens) * reps / dt / 1e12, 6), "unit": "TFLOP/s",
+           "cores": int(blas_threads()), "kind": kind, "seconds": round(dt, 2),
+           "sample": f"LLaMA FFN gate+up+down step (V=64 2:4, identical encodings), {reps} x {tokens} "
+                     f"tokens, {what}, float64; host cpu_count={os.cpu_count()}"}
+    if hinm is not None:
+        out["cfg1"] = reference_cfg1(hinm)
+    return out
+
+
+def reference_cfg1(hinm):
+    """BASELINE configs[0] on the host cores: 768x3072 BERT FFN layer, 512 tokens, V=64 2:4 at 75%,
+    the reference's full CPU path (vector_prune -> nm_prune -> encode -> hinm_spmm ->
+    restore_row_order).  sigma: the reference's gyro_permute with icp_max_iters=0 (its OCP phase;
+    the default ICP budget takes hours on this shape)."""
+    from paper_2407_20496_b200 import synth
+    from hinm.pruning import restore_row_order
+
+    m, n, B = 768, 3072, 512
+    W = synth.randn_bf16((m, n), 0).astype(np.float64)
+    X = synth.randn_bf16((n, B), 1).astype(np.float64)
+    cfg = hinm.HiNMConfig(vector_size=64, nm_keep=2, nm_group=4, vector_sparsity=0.5, icp_max_iters=0)
+    t0 = time.perf_counter()
+    sigma, masks, _ = hinm.gyro_permute(W, cfg)
+    t1 = time.perf_counter()
+    enc = hinm.encode(W, masks, sigma, cfg)
+    t2 = time.perf_counter()
+    restore_row_order(hinm.hinm_spmm(enc, X), enc.sigma_o)
+    t3 = time.perf_counter()
+    return {"shape": "768x3072 @ 512 tokens", "gyro_ocp_s": round(t1 - t0, 3),
+            "encode_s": round(t2 - t1, 3), "spmm_restore_s": round(t3 - t2, 3),
+            "spmm_tflops": round(2.0 * m * n * B / (t3 - t2) / 1e12, 6)}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle port on the same workload (bounded samples), rank 0 only."""
+    """--impl reference: the reference's own CPU path (oracle/_ref: vector_prune -> nm_prune ->
+    encode once, then hinm_spmm + restore_row_order per step) on the bench workload's three layers
+    at a bounded token sample, rank 0 only; the numpy oracle port when the package is absent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import hinm_oracle as O
     from paper_2407_20496_b200 import synth
 
-    try:
-        from threadpoolctl import threadpool_info
-        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-    except Exception:  # pragma: no cover
-        blas_threads = os.cpu_count()
-    m, n = N_FFN, M_FFN                          # down projection is the sample layer
-    W = synth.randn_bf16((m, n), 0).astype(np.float64)
-    so = synth.random_sigma_o(m, 2)
-    r = O.compress(W, so, V, NM_N, NM_M, (m // V) * int(n * (1 - SV)))
+    hinm = _reference_module()
+    _pool = all_host_threads()  # noqa: F841  (kept alive for the measurement)
     tokens = args.cpu_tokens
-    X = synth.randn_bf16((n, tokens), 1).astype(np.float64)
+    layers = {}
+    rng_seed = 0
+    for name, m, n in layer_shapes():
+        W = synth.randn_bf16((m, n), rng_seed).astype(np.float64)
+        so = synth.random_sigma_o(m, rng_seed + 1)
+        rng_seed += 2
+        if hinm is not None:
+            from hinm.pruning import survivors_per_tile
+            cfg = hinm.HiNMConfig(vector_size=V, nm_keep=NM_N, nm_group=NM_M, vector_sparsity=SV)
+            S = hinm.magnitude_saliency(W)
+            vm = hinm.vector_prune(S, cfg, so)
+            sigma = hinm.GyroPermutation(sigma_o=so, sigma_i=tuple(survivors_per_tile(vm)))
+            em = hinm.nm_prune(S, vm, cfg, sigma)
+            layers[name] = hinm.encode(W, hinm.MaskPair(vector_mask=vm, element_mask=em), sigma, cfg)
+        else:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import hinm_oracle as O
+            layers[name] = (O.compress(W, so, V, NM_N, NM_M, (m // V) * int(n * (1 - SV)))["tiles"], so)
+    X = synth.randn_bf16((N_FFN, tokens), 99).astype(np.float64)
+
+    if hinm is not None:
+        from hinm.pruning import restore_row_order
+
+        def spmm(name, x):
+            e = layers[name]
+            return restore_row_order(hinm.hinm_spmm(e, x), e.sigma_o)
+        kind, what = "reference", "oracle/_ref (unmodified hinm package): hinm_spmm + restore_row_order"
+    else:
+        import hinm_oracle as O
+
+        def spmm(name, x):
+            t, so = layers[name]
+            m = so.size
+            return O.restore_row_order(O.hinm_spmm(t, x, m, V, NM_N, NM_M), so)
+        kind, what = "port", "oracle/hinm_oracle.py (numpy port of the reference)"
 
     def one():
-        Y = O.hinm_spmm(r["tiles"], X, m, V, NM_N, NM_M)
-        O.restore_row_order(Y, so)
+        spmm("gate", X)
+        up = spmm("up", X)
+        spmm("down", up)
 
     for _ in range(min(args.warmup, 1)):
         one()
@@ -412,22 +693,127 @@ def run_reference(args):
     for _ in range(args.steps):
         one()
     dt = (time.perf_counter() - t0) / args.steps
-    value = 2.0 * m * n * tokens / dt / 1e12
+    value = eff_flops(tokens) / dt / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "LLaMA-7B FFN down projection sample (4096x11008, V=64 2:4, "
-                               f"{tokens} tokens) of the bench workload"},
-        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": int(blas_threads),
-                         "kind": "port",
-                         "sample": f"oracle hinm_spmm + restore_row_order, {tokens} tokens per step"},
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) bf16-valued weights/activations, random sigma_o)",
+        "config": {"workload": f"LLaMA-7B FFN layer (gate+up 11008x4096, down 4096x11008), 75% HiNM "
+                               f"V=64 2:4 s_v=0.5, {tokens}-token sample of the bench workload per step"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": int(blas_threads()),
+                         "kind": kind,
+                         "sample": f"{what}; gate+up+down at {tokens} tokens per step; compression "
+                                   "by the same package outside the timed region"},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# secondary configurations (BASELINE configs[0], [1], [3], [4]): one JSON line each
+def cfg_cases(name):
+    """[(label, m, n, tokens, V, s_v, count, graph)] of a BASELINE configuration."""
+    if name == "cfg1":
+        return [("ffn1", 768, 3072, 512, 64, 0.5, 1, True), ("ffn2", 3072, 768, 512, 64, 0.5, 1, True)]
+    if name == "cfg2":
+        return [("qkvo", 768, 768, 4096, 64, 0.5, 48, True), ("ffn1", 3072, 768, 4096, 64, 0.5, 12, True),
+                ("ffn2", 768, 3072, 4096, 64, 0.5, 12, True)]
+    if name in ("cfg4", "cfg4_875"):
+        sv = 0.5 if name == "cfg4" else 0.75
+        shapes = [(64, 64, 802816, 1), (64, 576, 802816, 3), (256, 64, 802816, 4), (64, 256, 802816, 2),
+                  (128, 256, 802816, 1), (128, 1152, 200704, 4), (512, 128, 200704, 4),
+                  (512, 256, 200704, 1), (128, 512, 200704, 3), (256, 512, 200704, 1),
+                  (256, 2304, 50176, 6), (1024, 256, 50176, 6), (1024, 512, 50176, 1),
+                  (256, 1024, 50176, 5), (512, 1024, 50176, 1), (512, 4608, 12544, 3),
+                  (2048, 512, 12544, 3), (2048, 1024, 12544, 1), (512, 2048, 12544, 2)]
+        return [(f"{m}x{n}", m, n, tok, 64, sv, c, False) for m, n, tok, c in shapes
+                if (n * (1 - sv)) % 4 == 0]
+    if name == "cfg5":
+        return [(f"V{v}_keep{int(100 * (1 - sv))}", 4096, 4096, 16384, v, sv, 1, False)
+                for v in (32, 64, 128) for sv in (0.5, 0.75)]
+    raise ValueError(name)
+
+
+def run_config(args):
+    import torch
+
+    import paper_2407_20496_b200 as H
+    from paper_2407_20496_b200.shard import shard_bounds
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d = Dist("nccl", dev)
+    rows, tot_sp, tot_cb, tot_f, launches = [], 0.0, 0.0, 0.0, 0
+    flush = l2_flush_buffer(torch, dev)
+
+    def timed(fn, graph):
+        """per-call device time, max over ranks: eager (events around K calls, L2 flushed before the
+        timed region) or one CUDA graph of K calls for the latency-bound shapes"""
+        torch.cuda.synchronize()
+        time.sleep(0.3)
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                fn()
+            torch.cuda.current_stream().wait_stream(st)
+            with torch.cuda.graph(g):
+                for _ in range(args.steps):
+                    fn()
+            g.replay()
+            run = g.replay
+        else:
+            def run():
+                for _ in range(args.steps):
+                    fn()
+        flush.fill_(1)
+        d.barrier()
+        torch.cuda.synchronize()
+        s, e = _events(torch, 2)
+        s.record()
+        run()
+        e.record()
+        torch.cuda.synchronize()
+        return d.max(s.elapsed_time(e), dev) / args.steps
+
+    for i, (label, m, n, tokens, v, sv, count, graph) in enumerate(cfg_cases(args.config)):
+        lo, hi = shard_bounds(tokens, d.world, d.rank)
+        tl = hi - lo
+        g = torch.Generator(device=dev).manual_seed(31 + i)
+        W = torch.randn(m, n, generator=g, device=dev).to(torch.bfloat16)
+        X = torch.randn(n, tl, generator=g, device=dev).to(torch.bfloat16)
+        Y = torch.empty(m, tl, dtype=torch.bfloat16, device=dev)
+        Yc = torch.empty(m, tl, dtype=torch.bfloat16, device=dev)
+        pack = H.compress(W, H.HiNMConfig(v, 2, 4, sv), np.random.default_rng(i).permutation(m))
+        ms = timed(lambda: H.spmm(pack, X, out=Y, order="original"), graph)
+        cb = timed(lambda: torch.matmul(W, X, out=Yc), graph)
+        f = 2.0 * m * n * tokens
+        launches += count * args.steps
+        rows.append({"gemm": label, "m": m, "n": n, "tokens": tokens, "V": v, "s_v": sv, "count": count,
+                     "spmm_ms": round(ms, 4), "cublas_ms": round(cb, 4), "speedup": round(cb / ms, 3),
+                     "eff_tflops": round(f / ms / 1e9, 1), "timing": "cuda graph" if graph else "eager"})
+        tot_sp += ms * count
+        tot_cb += cb * count
+        tot_f += f * count
+        del W, X, Y, Yc, pack
+    if d.rank == 0:
+        print(json.dumps({
+            "metric": f"HiNM SpMM effective TFLOPS ({args.config})", "value": round(tot_f / tot_sp / 1e9, 2),
+            "unit": "TFLOP/s", "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot_sp, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": args.config, "l2": "flushed (512 MB write) before each timed region"},
+            "speedup_vs_cublas": round(tot_cb / tot_sp, 3), "cublas_ms_per_step": round(tot_cb, 4),
+            "gpu_launches": launches, "rows": rows}), flush=True)
+    d.close()
 
 
 def main():
@@ -436,18 +822,33 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-tokens", type=int, default=64)
+    ap.add_argument("--config", default="llama", choices=["llama", "cfg1", "cfg2", "cfg4", "cfg4_875", "cfg5"])
+    ap.add_argument("--tokens", type=int, default=GLOBAL_TOKENS, help="global tokens (per GPU with --weak)")
+    ap.add_argument("--v", type=int, default=V, choices=[32, 64, 128], help="vector size of the llama step")
+    ap.add_argument("--weak", action="store_true", help="weak scaling: --tokens per rank (default: "
+                                                        "strong, --tokens split over the ranks)")
+    ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: 16384 global tokens split over the ranks (default: weak, "
-                         "16384 tokens per rank)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the V=128 secondary row")
+    ap.add_argument("--dry-run", action="store_true", help="CPU plumbing check (gloo, no kernels)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+        return
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    world = int(world_env or 1)
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        run_dry(args)
+    elif args.config == "llama":
+        run_llama(args)
     else:
-        run_ours(args)
+        run_config(args)
 
 
 if __name__ == "__main__":

@@ -132,10 +132,19 @@ __global__ void k_gains(const double* __restrict__ sorted, int n, int M, int G, 
   }
 }
 
-// Orderable key: ascending key <=> descending gain (gains are >= +0.0 after canonicalisation).
-__device__ __forceinline__ uint64_t gain_key(double g) {
-  return ~(uint64_t)__double_as_longlong(g);
+// Order-preserving map of a double onto uint64 (any sign: external saliency may be negative, as
+// the reference's lexsort on -score allows): negative values have every bit flipped, the others
+// only the sign bit.  -0.0 never reaches it (scores and gains are canonicalised with + 0.0).
+__device__ __forceinline__ uint64_t ord_key(double d) {
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  return b ^ ((b >> 63) ? ~0ull : (1ull << 63));
 }
+__device__ __forceinline__ double ord_value(uint64_t k) {
+  return __longlong_as_double((long long)(k ^ ((k >> 63) ? (1ull << 63) : ~0ull)));
+}
+
+// Budget key: ascending key <=> descending gain.
+__device__ __forceinline__ uint64_t gain_key(double g) { return ~ord_key(g); }
 
 // #{q : key(t,q) <= x} (upper) or < x (lower) for a non-decreasing key row.
 __device__ int row_bound(const double* row, int G, uint64_t x, bool upper) {
@@ -194,8 +203,8 @@ __device__ int64_t block_sum64(int64_t v, int64_t* red) {
 
 // a4 (fast path, n <= 16384): one CTA per tile sorts the tile's scores in registers/smem with a
 // stable block radix sort (descending keys; input in column order => ties keep the lower
-// column first, == np.lexsort((cols, -score))).  Scores are >= +0.0, so their IEEE bit patterns
-// order like the values; only the bits that differ inside the tile are sorted (column sums of
+// column first, == np.lexsort((cols, -score))).  Keys are the order-preserving uint64 images of the
+// scores (ord_key); only the bits that differ inside the tile are sorted (column sums of
 // bf16 magnitudes share their top exponent bits and end in long runs of zero mantissa bits:
 // ~32 of 64 bits vary on N(0,1) weights, 6 radix passes instead of 11).
 struct OrOp {
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const doubl
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int j = threadIdx.x * ITEMS + i;  // blocked arrangement = column order
-    keys[i] = j < n ? (uint64_t)__double_as_longlong(row[j]) : 0ull;
+    keys[i] = j < n ? ord_key(row[j]) : 0ull;
     vals[i] = j;
     if (j < n) { lor |= keys[i]; land &= keys[i]; }
   }
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const doubl
   for (int i = 0; i < ITEMS; ++i) {
     const int j = threadIdx.x * ITEMS + i;
     if (j < n) {
-      sorted[(int64_t)t * n + j] = __longlong_as_double((long long)keys[i]);
+      sorted[(int64_t)t * n + j] = ord_value(keys[i]);
       order[(int64_t)t * n + j] = vals[i];
     }
   }

@@ -27,6 +27,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <initializer_list>
 #include <mutex>
 #include <vector>
 
@@ -68,6 +69,8 @@ struct Params {
   int units;
   int out_order;
   int y_align32;      // Y rows 32-byte aligned: 256-bit stores
+  uint32_t xpitch;    // bytes between consecutive K-rows (channels) of X
+  int64_t xblk;       // bytes between consecutive BNT-token blocks of X
 };
 
 struct SmemLayout {
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
       ps = 0;
     };
     next_unit();
-    const uint32_t ldx2 = (uint32_t)(ldx * 2);  // row pitch in bytes (host: < 2^32)
+    const uint32_t ldx2 = p.xpitch;  // row pitch in bytes (host: < 2^32)
     uint32_t r_row[PF];
     int r_col[PF], r_n[PF];
     bool r_ok[PF];
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         // scarce resource, ncu source view); rows < 64 always exist, the rest only in full stages
         const int tok = r_col[j] + lpos * 8;
         const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-        const char* xs = xbase + (src_bytes ? tok * 2 : 0);
+        const char* xs = xbase + (src_bytes ? (int64_t)(r_col[j] / BNT) * p.xblk + lpos * 16 : 0);
         const uint32_t my_row = r_row[j];
         const bool full = r_n[j] == KS;
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
@@ -793,36 +796,72 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   prm.T = pk->T;
   prm.V = pk->V;
   prm.out_order = out_order;
-  static const int env_v8 = getenv("HINM_Y_V8") ? atoi(getenv("HINM_Y_V8")) : 1;
-  prm.y_align32 = env_v8 && (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
-  // Configuration.  Defaults (B200 measurements, scripts/spmm_grid.sh): 8 gather warps (16 are no
-  // faster: the fill rate under a running MMA is the cap); V <= 64 -> 128-row X stages; V = 128 -> 64-row
-  // X stages (its 8 KB A stages need the deeper A ring that the smaller X ring leaves room for).
-  // Unit width BNT: 256 tokens.  BNT = 128 (two accumulators: the drain of one unit overlaps the
-  // next unit's MMAs, twice the units) is slower whenever the 256-token units fill the machine,
-  // small-K shapes included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @ 802816
-  // 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is re-read
-  // twice as often.  It is used only when the units would otherwise leave SMs idle.
-  // Experiments: HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_PDL = 0 | 1,
-  // HINM_GATHER = m128 (M=128 instruction for V <= 64) | dbg_nomma | dbg_nogather | dbg_noepi |
-  // dbg_gather_x_only | dbg_gather_sparse | dbg_pad_quarter | dbg_half_a (timing only: results are
-  // garbage; see the DBG note above the kernel).
-  static const int env_ks = getenv("HINM_KS") ? atoi(getenv("HINM_KS")) : 0;
-  static const int env_gw = getenv("HINM_GW") ? atoi(getenv("HINM_GW")) : 0;
-  static const int env_bn = getenv("HINM_BN") ? atoi(getenv("HINM_BN")) : 0;
-  static const int variant = [] {
-    const char* e = getenv("HINM_GATHER");
-    if (!e) return 0;
-    if (!strcmp(e, "m128")) return 1;
-    if (!strcmp(e, "dbg_nomma")) return 2;
-    if (!strcmp(e, "dbg_nogather")) return 3;
-    if (!strcmp(e, "dbg_noepi")) return 4;
-    if (!strcmp(e, "dbg_gather_x_only")) return 5;
-    if (!strcmp(e, "dbg_gather_sparse")) return 6;  // gather only, every 4th row's bytes skipped
-    if (!strcmp(e, "dbg_pad_quarter")) return 7;    // full kernel, every 4th row unfetched (padding)
-    if (!strcmp(e, "dbg_half_a")) return 8;         // full kernel, A image loaded for even token blocks only
-    return 0;
+  // Tuning knobs (environment; every value is validated, an unknown one is an error rather than a
+  // silent default).  Defaults are the B200 measurements (scripts/spmm_grid.sh): 8 gather warps (16
+  // are no faster: the fill rate under a running MMA is the cap); V <= 64 -> 128-row X stages;
+  // V = 128 -> 64-row X stages (its 8 KB A stages need the deeper A ring that the smaller X ring
+  // leaves room for).  Unit width BNT: 256 tokens.  BNT = 128 (two accumulators: the drain of one
+  // unit overlaps the next unit's MMAs, twice the units) is slower whenever the 256-token units
+  // fill the machine, small-K shapes included (3072x768 @ 4096 tokens 0.024 -> 0.028 ms, 256x64 @
+  // 802816 0.10 -> 0.12 ms): 256-byte row segments gather less efficiently and the A image is
+  // re-read twice as often.  It is used only when the units would otherwise leave SMs idle.
+  //   HINM_BN = 128 | 256, HINM_KS = 64 | 128, HINM_GW = 8 | 16, HINM_PDL = 0 | 1, HINM_Y_V8 = 0 | 1,
+  //   HINM_GATHER = m128 (the M=128 instruction for V <= 64).
+  // Timing-only variants (results are garbage: see the DBG note above the kernel) exist only in the
+  // experiments build (-DHINM_EXPERIMENTS, scripts/ only): HINM_GATHER = dbg_nomma | dbg_nogather |
+  // dbg_noepi | dbg_gather_x_only | dbg_gather_sparse | dbg_pad_quarter | dbg_half_a, HINM_XBLK = 1.
+  struct Knobs {
+    int v8, ks, gw, bn, pdl, variant, xblk;
+    bool ok;
+  };
+  static const Knobs kn = [] {
+    Knobs k{1, 0, 0, 0, -1, 0, 0, true};
+    auto num = [&k](const char* name, int* dst, std::initializer_list<int> allowed) {
+      const char* e = getenv(name);
+      if (!e) return;
+      char* endp = nullptr;
+      const long v = strtol(e, &endp, 10);
+      bool good = endp && *endp == 0 && endp != e;
+      if (good) {
+        good = false;
+        for (int a : allowed) good |= v == a;
+      }
+      if (!good) {
+        fprintf(stderr, "[hinm] invalid %s=%s\n", name, e);
+        k.ok = false;
+        return;
+      }
+      *dst = (int)v;
+    };
+    num("HINM_Y_V8", &k.v8, {0, 1});
+    num("HINM_KS", &k.ks, {64, 128});
+    num("HINM_GW", &k.gw, {8, 16});
+    num("HINM_BN", &k.bn, {128, 256});
+    num("HINM_PDL", &k.pdl, {0, 1});
+    if (const char* e = getenv("HINM_GATHER")) {
+      static const char* names[] = {"m128", "dbg_nomma", "dbg_nogather", "dbg_noepi", "dbg_gather_x_only",
+                                    "dbg_gather_sparse", "dbg_pad_quarter", "dbg_half_a"};
+      int v = -1;
+      for (int i = 0; i < 8; ++i)
+        if (!strcmp(e, names[i])) v = i + 1;
+#ifndef HINM_EXPERIMENTS
+      if (v > 1) v = -1;  // timing-only variants are not part of the product library
+#endif
+      if (v < 0) {
+        fprintf(stderr, "[hinm] invalid HINM_GATHER=%s\n", e);
+        k.ok = false;
+      } else {
+        k.variant = v;
+      }
+    }
+#ifdef HINM_EXPERIMENTS
+    num("HINM_XBLK", &k.xblk, {0, 1});
+#endif
+    return k;
   }();
+  if (!kn.ok) return HINM_ERR_VALUE;
+  prm.y_align32 = kn.v8 && (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
+  const int variant = kn.variant;
   const int dev = current_device();
   const int sms = sm_count(dev);
   // 128-token units only when 256-token units would leave more than half the SMs idle (e.g. the
@@ -830,9 +869,15 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   // 0.030 -> 0.024 ms); with more units the 256-token kernel wins
   const int64_t units256 = (int64_t)((B + 255) / 256) * pk->T;
   int bnt = units256 * 2 <= sms ? 128 : 256;
-  if (env_bn == 128 || env_bn == 256) bnt = env_bn;
-  if (variant >= 2) bnt = 256;
+  if (kn.bn) bnt = kn.bn;
+  if (variant >= 2 || kn.xblk) bnt = 256;
   prm.units = ((B + bnt - 1) / bnt) * pk->T;
+  prm.xpitch = (uint32_t)(ldx * 2);
+  prm.xblk = (int64_t)bnt * 2;
+  if (kn.xblk) {  // experiment: X stored token-block-major, [B/256][n][256]
+    prm.xpitch = 512;
+    prm.xblk = (int64_t)pk->n * 512;
+  }
   const int grid = std::min(prm.units, sms);
   cudaStream_t st = (cudaStream_t)stream;
   const bool m64 = pk->V <= 64 && variant != 1;
@@ -840,8 +885,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   // (layer chains, CUDA graphs) overlap this kernel's prologue with the previous kernel's tail,
   // ~1-1.7 us per launch on the BERT / cfg1 shapes (scripts/small_shapes.py).  Long kernels (more
   // than 8 units per SM) gain nothing measurable and keep plain launches (HINM_PDL = 0 | 1 forces).
-  static const int env_pdl = getenv("HINM_PDL") ? atoi(getenv("HINM_PDL")) : -1;
-  const bool pdl = env_pdl == 1 || (env_pdl == -1 && prm.units <= 8 * sms);
+  const bool pdl = kn.pdl == 1 || (kn.pdl == -1 && prm.units <= 8 * sms);
   auto launch = [&](auto kern, int ks, int gw, int bn) -> int {
     const SmemLayout L = smem_layout(pk->V, ks, m64, bn);
     HINM_CUDA_TRY(ensure_smem((const void*)kern, dev, (int)L.total));
@@ -858,9 +902,10 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     HINM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, X, ldx, prm));
     return HINM_OK;
   };
-  const int ks = env_ks == 64 || env_ks == 128 ? env_ks : (pk->V <= 64 ? 128 : 64);
-  const int gw = env_gw == 8 || env_gw == 16 ? env_gw : 8;
+  const int ks = kn.ks ? kn.ks : (pk->V <= 64 ? 128 : 64);
+  const int gw = kn.gw ? kn.gw : 8;
   int rc;
+#ifdef HINM_EXPERIMENTS
   if (variant == 2) {
     rc = gw == 16 ? launch(k_hinm_spmm<128, 16, 1, true>, 128, 16, 256) : launch(k_hinm_spmm<128, 8, 1, true>, 128, 8, 256);
   } else if (variant == 3) {
@@ -875,7 +920,9 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     rc = m64 ? launch(k_hinm_spmm<128, 8, 6, true>, 128, 8, 256) : launch(k_hinm_spmm<64, 8, 6, false>, 64, 8, 256);
   } else if (variant == 8) {
     rc = launch(k_hinm_spmm<128, 8, 7, true>, 128, 8, 256);
-  } else if (bnt == 128) {
+  } else
+#endif
+  if (bnt == 128) {
     rc = ks == 128 ? (m64 ? launch(k_hinm_spmm<128, 8, 0, true, 128>, 128, 8, 128)
                           : launch(k_hinm_spmm<128, 8, 0, false, 128>, 128, 8, 128))
                    : (m64 ? launch(k_hinm_spmm<64, 8, 0, true, 128>, 64, 8, 128)

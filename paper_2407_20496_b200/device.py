@@ -190,10 +190,11 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
     m, n = weights.shape
     vcfg = ensure_validated(cfg, (m, n))
     dev = weights.device
+    from .pruning import check_sigma_o
+
+    check_sigma_o(sigma_o, m)
     so = torch.from_numpy(np.ascontiguousarray(sigma_o, dtype=np.int32)).to(dev) if not (
         hasattr(sigma_o, "is_cuda")) else sigma_o.to(device=dev, dtype=torch.int32)
-    if so.numel() != m:
-        raise ShapeMismatch(f"sigma_o has {so.numel()} entries, weights have {m} rows")
     pack = _empty_pack(vcfg, dev)
     pack.sigma_o = so.contiguous()
     if build_operand_image is None:
@@ -249,7 +250,8 @@ def spmm(pack: DevicePack, X, out=None, order: str = "sigma"):
     """tcgen05 HiNM SpMM: Y (m x B, bf16) = W_hinm @ X (n x B, bf16, channel-major).
 
     ``order='sigma'`` returns rows in sigma_o order (== hinm.hinm_spmm); ``'original'`` fuses
-    restore_row_order into the epilogue store.
+    restore_row_order into the epilogue store.  ``out`` (optional) must be an (m x B) bf16 CUDA
+    tensor with contiguous rows on X's device.
     """
     torch = _torch()
     _require_cuda(X, "inputs")
@@ -259,31 +261,51 @@ def spmm(pack: DevicePack, X, out=None, order: str = "sigma"):
         raise ShapeMismatch(f"input has {X.shape[0]} rows, encoding expects {pack.n}")
     if not pack.has_operand_image:
         raise ValueError("pack has no tcgen05 operand image (needs 2:4 and V in 32/64/128)")
+    if pack.device != X.device:
+        raise ValueError(f"pack is on {pack.device}, inputs on {X.device}")
+    if order not in ("sigma", "original"):
+        raise ValueError(f"order must be 'sigma' or 'original', got {order!r}")
     B = X.shape[1]
     if out is None:
         out = torch.empty(pack.m, B, dtype=torch.bfloat16, device=X.device)
+    elif (not getattr(out, "is_cuda", False) or out.device != X.device or out.dtype != torch.bfloat16
+          or tuple(out.shape) != (pack.m, B) or out.stride(1) != 1):
+        raise ValueError(f"out must be a ({pack.m}, {B}) bfloat16 tensor on {X.device} with "
+                         "contiguous rows")
     ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
     st = pack.struct()
     lib = _lib.load()
-    status = lib.hinm_spmm_bf16(ctypes.byref(st), X.data_ptr(), X.stride(0), B, out.data_ptr(),
-                                out.stride(0), ordv, _stream_handle(X.device))
+    dev = X.device.index
+    if dev != torch.cuda.current_device():
+        with torch.cuda.device(dev):
+            status = lib.hinm_spmm_bf16(ctypes.byref(st), X.data_ptr(), X.stride(0), B,
+                                        out.data_ptr(), out.stride(0), ordv, _stream_handle(dev))
+    else:
+        status = lib.hinm_spmm_bf16(ctypes.byref(st), X.data_ptr(), X.stride(0), B, out.data_ptr(),
+                                    out.stride(0), ordv, _stream_handle(dev))
     _lib.check(status, "spmm")
     return out
 
 
 def spmm_simt(pack: DevicePack, X, order: str = "sigma"):
-    """Cross-check product on CUDA cores from the reference view (fp32 out)."""
+    """The same product on CUDA cores from the reference view (fp32 out): any V and N:M.
+
+    Not a performance path -- it is the cross-check kernel of the tests and the kernel behind
+    hinm_spmm for encodings the tcgen05 kernel does not cover (see spmm.hinm_spmm)."""
     torch = _torch()
     _require_cuda(X, "inputs")
     if X.shape[0] != pack.n:
         raise ShapeMismatch(f"input has {X.shape[0]} rows, encoding expects {pack.n}")
+    if pack.device != X.device:
+        raise ValueError(f"pack is on {pack.device}, inputs on {X.device}")
     B = X.shape[1]
     out = torch.zeros(pack.m, B, dtype=torch.float32, device=X.device)
     ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
     st = pack.struct()
-    _lib.check(_lib.load().hinm_spmm_simt_f32(ctypes.byref(st), X.data_ptr(), X.stride(0), B,
-                                              out.data_ptr(), out.stride(0), ordv,
-                                              _stream_handle(X.device)), "spmm_simt")
+    with torch.cuda.device(X.device):
+        _lib.check(_lib.load().hinm_spmm_simt_f32(ctypes.byref(st), X.data_ptr(), X.stride(0), B,
+                                                  out.data_ptr(), out.stride(0), ordv,
+                                                  _stream_handle(X.device)), "spmm_simt")
     return out
 
 

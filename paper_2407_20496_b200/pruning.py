@@ -55,6 +55,39 @@ def _dev_i32(x, torch, device):
     return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.int64)).astype(np.int32)).to(device)
 
 
+def check_sigma_o(sigma_o, m: int) -> None:
+    """Host-side guard before any kernel indexes W with sigma_o: ShapeMismatch for a wrong
+    length, IndexError for an entry outside [0, m) (the reference's fancy index ``S[rows]``,
+    pruning.py:63-80, raises IndexError there).  CUDA tensors are checked with one reduction."""
+    if _is_cuda(sigma_o):
+        n = sigma_o.numel()
+        lo = int(sigma_o.min()) if n else 0
+        hi = int(sigma_o.max()) if n else -1
+    else:
+        a = np.asarray(sigma_o)
+        if a.ndim != 1:
+            raise ShapeMismatch(f"sigma_o must be 1-D, got shape {a.shape}")
+        n = a.size
+        lo = int(a.min()) if n else 0
+        hi = int(a.max()) if n else -1
+    if n != m:
+        raise ShapeMismatch(f"sigma_o has {n} entries for {m} rows")
+    if lo < 0 or hi >= m:
+        raise IndexError(f"sigma_o entry {lo if lo < 0 else hi} out of range for {m} rows")
+
+
+def _check_scores(saliency, S) -> None:
+    """Raw score arrays may hold any real value (the reference sorts -score with lexsort, and the
+    device keys are order-preserving for negatives); NaN / Inf have no reference order here and
+    are rejected.  SaliencyMatrix inputs were already checked by their constructor."""
+    if isinstance(saliency, SaliencyMatrix):
+        return
+    import torch
+
+    if not bool(torch.isfinite(S).all()):
+        raise ValueError("saliency contains NaN or infinite values")
+
+
 def _sigma_csr(sigma_i, T, torch, device):
     sizes = [int(np.asarray(s).size) for s in sigma_i]
     if len(sizes) != T:
@@ -94,9 +127,9 @@ def vector_prune(saliency, cfg, sigma_o):
     m, n = S.shape
     vcfg = ensure_validated(cfg, (m, n))
     dev = S.device
+    _check_scores(saliency, S)
+    check_sigma_o(sigma_o, m)
     so = _dev_i32(sigma_o, torch, dev)
-    if so.numel() != m:
-        raise ShapeMismatch(f"sigma_o has {so.numel()} entries for {m} rows")
     lib = _lib.load()
     wsb = ctypes.c_size_t()
     _lib.check(lib.hinm_compress_workspace(m, n, vcfg.vector_size, vcfg.nm_group,
@@ -129,6 +162,8 @@ def nm_prune(saliency, vector_mask, cfg, sigma: GyroPermutation):
           torch.as_tensor(np.asarray(vector_mask, dtype=bool))).to(device=dev, dtype=torch.uint8)
     if tuple(vm.shape) != (T, n):
         raise InvariantViolation(f"vector mask shape {tuple(vm.shape)} unexpected")
+    _check_scores(saliency, S)
+    check_sigma_o(sigma.sigma_o, m)
     so = _dev_i32(sigma.sigma_o, torch, dev)
     sp, si, _ = _sigma_csr(sigma.sigma_i, T, torch, dev)
     em = torch.zeros(m, n, dtype=torch.uint8, device=dev)

@@ -1,13 +1,16 @@
 """Drop-in replacement for the reference's SpMM API (pkg/src/hinm/spmm.py).
 
 ``hinm_spmm(enc, X)`` (spmm.py:75-99) runs the tcgen05 kernel for 2:4 encodings with
-V in {32, 64, 128} (the hot path); other N:M / V encodings run the CUDA-core kernel.
-Both are GPU kernels -- there is no CPU fallback.  Host inputs are computed in bf16 with fp32
+V in {32, 64, 128} -- the performance path.  The reference API also accepts any
+other N:M / V encoding (its KATs use V in {1, 2, 4}, N:M 1:1 / 1:2); those run on the CUDA-core
+reference-view kernel (``spmm_simt``), which exists for parity, not speed, and hinm_spmm says so
+with a one-time ``HiNMPerformanceWarning``.  Both are GPU kernels -- there is no CPU fallback.  Host inputs are computed in bf16 with fp32
 accumulation (north-star tolerance rtol 1e-2 / atol 1e-3) and returned as float64 numpy.
 """
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -38,6 +41,23 @@ def gather_tile_buffer(tile: TileEncoding, inputs) -> TileBuffer:
     return TileBuffer(rows=X[idx])
 
 
+class HiNMPerformanceWarning(UserWarning):
+    """An encoding outside the tcgen05 kernel's configs (2:4, V in {32, 64, 128}) ran on the
+    CUDA-core parity kernel."""
+
+
+_warned_general = False
+
+
+def _warn_general(pack) -> None:
+    global _warned_general
+    if not _warned_general:
+        _warned_general = True
+        warnings.warn(f"hinm_spmm: V={pack.V} {pack.N}:{pack.M} is outside the tcgen05 kernel "
+                      "(2:4, V in 32/64/128); running the CUDA-core parity kernel",
+                      HiNMPerformanceWarning, stacklevel=3)
+
+
 def _run(pack: DevicePack, inputs, order: str):
     torch = _torch()
     on_dev = _is_cuda(inputs)
@@ -60,6 +80,7 @@ def _run(pack: DevicePack, inputs, order: str):
             Xb = Xp
         Y = _spmm_tc(pack, Xb, order=order)[:, :B]
     else:
+        _warn_general(pack)
         Y = _spmm_simt(pack, X.to(torch.bfloat16).contiguous(), order=order)
     if on_dev:
         return Y
