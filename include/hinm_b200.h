@@ -15,6 +15,8 @@
  *   hinm_spmm_bf16      <- hinm.hinm_spmm(enc, X)                           spmm.py:75-99
  *                          + restore_row_order (out_order=ORIGINAL)        pruning.py:356-360
  *   hinm_spmm_simt_f32  <- same product on CUDA cores (cross-check kernel, not the product path)
+ *   hinm_unpack_to_reference <- HiNMEncoding / TileEncoding arrays (pruning.py:261-281) from a pack,
+ *                          decoding the tcgen05 operand image (parity of the bytes the MMA reads)
  *
  * Conventions
  *   - All array arguments are DEVICE pointers owned by the caller; the library never
@@ -56,6 +58,9 @@ enum { HINM_ORDER_SIGMA = 0, HINM_ORDER_ORIGINAL = 1 };
 
 /* Selection source for hinm_nm_select. */
 enum { HINM_SELECT_SCORES = 0, HINM_SELECT_MASK = 1 };
+
+/* Source of hinm_unpack_to_reference. */
+enum { HINM_UNPACK_REFERENCE_VIEW = 0, HINM_UNPACK_OPERAND_IMAGE = 1 };
 
 /*
  * Device pack of one HiNM-encoded matrix.
@@ -138,15 +143,18 @@ int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const double* Wd, i
 int hinm_pack_build(hinm_pack_t* pack, void* stream);
 
 /*
- * Fused compressor (north-star subsystem 1): W bf16 + sigma_o (+ optional sigma_i CSR)
- * -> complete pack (reference view + operand image).  `pack` buffers are caller-allocated
- * with the capacities above; sig_ptr/sig_idx NULL selects ascending survivors.
- * Synchronizing (sigma_i validation).
+ * Fused compressor (north-star subsystem 1; the `hinm encode --permutation [--saliency]` chain,
+ * cli.py:185-194): W bf16 + sigma_o (+ optional sigma_i CSR) -> complete pack (reference view +
+ * operand image).  Scores are |W| when `saliency` is NULL, else the caller's fp64 scores
+ * (m x n, leading dim lds; any real values -- load_saliency, pruning.py:42-54, feeding
+ * vector_prune / nm_prune as in cli.py:189-190); the kept values always come from W.  `pack`
+ * buffers are caller-allocated with the capacities above; sig_ptr/sig_idx NULL selects ascending
+ * survivors.  Synchronizing only when a caller sigma_i is validated.
  */
-int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t* sigma_o,
-                       const int32_t* sig_ptr, const int32_t* sig_idx, hinm_pack_t* pack,
-                       uint8_t* vector_mask_scratch, void* workspace, size_t workspace_bytes,
-                       void* stream);
+int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* saliency, int64_t lds,
+                       const int32_t* sigma_o, const int32_t* sig_ptr, const int32_t* sig_idx,
+                       hinm_pack_t* pack, uint8_t* vector_mask_scratch, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /*
  * HiNM SpMM on tcgen05 (north-star subsystems 2+3): Y = W_hinm @ X, bf16 in, fp32 accumulate
@@ -183,6 +191,16 @@ int hinm_chain_run_host(const hinm_chain_step_t* steps, int nsteps, const int64_
 /* Same product from the reference view on CUDA cores, fp32 out (test cross-check). Async. */
 int hinm_spmm_simt_f32(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
                        float* Y, int64_t ldy, int out_order, void* stream);
+
+/*
+ * The reference view of `pack` in HOST memory, in the pack's flat layout (tile_ptr[T+1],
+ * vec_idx[K], nm_pos / kept (bf16 bits) [V*K/M*N], sigma_o[m]): HINM_UNPACK_REFERENCE_VIEW copies the
+ * reference-view arrays; HINM_UNPACK_OPERAND_IMAGE decodes the tcgen05 operand image instead (2:4,
+ * V in {32,64,128}) and checks its padding (HINM_ERR_INVARIANT / HINM_ERR_INDEX on a malformed
+ * image).  Synchronous.
+ */
+int hinm_unpack_to_reference(const hinm_pack_t* pack, int source, int32_t* tile_ptr, int32_t* vec_idx,
+                             uint8_t* nm_pos, uint16_t* kept, int32_t* sigma_o, void* stream);
 
 /* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
 int hinm_last_launch_count(void);

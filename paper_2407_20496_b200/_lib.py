@@ -33,6 +33,7 @@ STATUS_TO_EXCEPTION = {
 
 HINM_ORDER_SIGMA, HINM_ORDER_ORIGINAL = 0, 1
 HINM_SELECT_SCORES, HINM_SELECT_MASK = 0, 1
+HINM_UNPACK_REFERENCE_VIEW, HINM_UNPACK_OPERAND_IMAGE = 0, 1
 
 
 class PackStruct(ctypes.Structure):
@@ -69,8 +70,10 @@ _SIGNATURES = {
                         c_vp, c_int, c_int, c_int, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp,
                         c_vp], c_int),
     "hinm_pack_build": ([ctypes.POINTER(PackStruct), c_vp], c_int),
-    "hinm_compress_bf16": ([c_vp, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(PackStruct), c_vp, c_vp,
-                            c_size, c_vp], c_int),
+    "hinm_compress_bf16": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(PackStruct),
+                            c_vp, c_vp, c_size, c_vp], c_int),
+    "hinm_unpack_to_reference": ([ctypes.POINTER(PackStruct), c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp], c_int),
     "hinm_spmm_bf16": ([ctypes.POINTER(PackStruct), c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp],
                        c_int),
     "hinm_spmm_simt_f32": ([ctypes.POINTER(PackStruct), c_vp, c_i64, c_int, c_vp, c_i64, c_int,

@@ -1312,9 +1312,9 @@ extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
   return HINM_OK;
 }
 
-extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t* sigma_o,
-                                  const int32_t* sig_ptr, const int32_t* sig_idx, hinm_pack_t* p,
-                                  uint8_t* vmask, void* workspace, size_t workspace_bytes,
+extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* S, int64_t lds,
+                                  const int32_t* sigma_o, const int32_t* sig_ptr, const int32_t* sig_idx,
+                                  hinm_pack_t* p, uint8_t* vmask, void* workspace, size_t workspace_bytes,
                                   void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!p || !W || !sigma_o || !vmask) return HINM_ERR_VALUE;
@@ -1325,16 +1325,17 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const int32_t*
   const bool own_sigma = sig_idx == nullptr;
   int32_t* surv = own_sigma ? p->vec_idx : (int32_t*)((char*)workspace + L.surv_tmp);
   int32_t* tptr = p->tile_ptr;
-  st = hinm_vector_prune(W, ldw, nullptr, 0, nullptr, 0, sigma_o, p->m, p->n, p->V, p->M,
+  st = hinm_vector_prune(W, ldw, nullptr, 0, S, lds, sigma_o, p->m, p->n, p->V, p->M,
                          p->total_keep, tptr, surv, vmask, workspace, workspace_bytes, stream_);
   if (st) return st;
   const int32_t* sp = own_sigma ? tptr : sig_ptr;
   const int32_t* si = own_sigma ? surv : sig_idx;
   const size_t rsmem = (((size_t)p->n * 4 + 15) & ~size_t(15)) + (size_t)p->n * 2;
-  const bool fast = rsmem <= 200 * 1024 && p->M <= 32 && p->N <= 16;
+  // the |W| fast paths select on bf16 magnitudes; external scores use the general select
+  const bool fast = !S && rsmem <= 200 * 1024 && p->M <= 32 && p->N <= 16;
   if (!own_sigma || !fast) {
     // validates a caller-supplied sigma_i (and selects when the fast path does not apply)
-    st = hinm_nm_select(HINM_SELECT_SCORES, W, ldw, nullptr, 0, nullptr, 0, nullptr, sigma_o, vmask,
+    st = hinm_nm_select(HINM_SELECT_SCORES, W, ldw, nullptr, 0, S, lds, nullptr, sigma_o, vmask,
                         sp, si, p->m, p->n, p->V, p->N, p->M, -1, nullptr,
                         fast ? nullptr : p->nm_pos, fast ? nullptr : p->kept_bf16, nullptr, stream_);
     if (st) return st;

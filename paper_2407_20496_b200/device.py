@@ -113,13 +113,41 @@ class DevicePack:
                    (self.gidx, self.a_vals, self.a_meta) if t is not None)
 
     # -------------------------------------------------------------------- reference view
-    def to_host_tiles(self):
-        """[(vector_index int64, nm_index (V, G*N) int64, kept_values (V, G*N) float64)] per tile."""
+    def to_host_arrays(self, source: str = "view"):
+        """Flat reference-view arrays on the host through hinm_unpack_to_reference:
+        (tile_ptr int64, vec_idx int64, nm_pos int64, kept float64, sigma_o int64).
+        ``source='image'`` decodes the tcgen05 operand image the SpMM reads (gidx, a_vals,
+        a_meta) instead of copying the reference view."""
         torch = _torch()
-        tp = self.tile_ptr.cpu().numpy().astype(np.int64)
-        vi = self.vec_idx.cpu().numpy().astype(np.int64)
-        nm = self.nm_pos.cpu().numpy().astype(np.int64)
-        kv = self.kept.float().cpu().numpy().astype(np.float64)
+        T, L = self.T, self.V * (self.total_keep // self.M) * self.N
+        if not self.vec_idx.is_cuda:  # a host-resident pack (replication plumbing): plain copies
+            if source == "image":
+                raise ValueError("the operand image is decoded from a CUDA pack")
+            kept = self.kept[:L].float().numpy().astype(np.float64)
+            return (self.tile_ptr.numpy().astype(np.int64), self.vec_idx[:self.total_keep].numpy().astype(np.int64),
+                    self.nm_pos[:L].numpy().astype(np.int64), kept, self.sigma_o.numpy().astype(np.int64))
+        tp = np.empty(T + 1, np.int32)
+        vi = np.empty(max(self.total_keep, 1), np.int32)
+        nm = np.empty(max(L, 1), np.uint8)
+        kv = np.empty(max(L, 1), np.uint16)
+        so = np.empty(max(self.m, 1), np.int32)
+        src = _lib.HINM_UNPACK_OPERAND_IMAGE if source == "image" else _lib.HINM_UNPACK_REFERENCE_VIEW
+        if source == "image" and not self.has_operand_image:
+            raise ValueError("pack has no tcgen05 operand image")
+        st = self.struct()
+        with torch.cuda.device(self.device):
+            status = _lib.load().hinm_unpack_to_reference(
+                ctypes.byref(st), src, tp.ctypes.data, vi.ctypes.data, nm.ctypes.data, kv.ctypes.data,
+                so.ctypes.data, _stream_handle(self.device))
+        _lib.check(status, "unpack_to_reference")
+        kept = (kv[:L].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        return (tp.astype(np.int64), vi[:self.total_keep].astype(np.int64), nm[:L].astype(np.int64),
+                kept, so[:self.m].astype(np.int64))
+
+    def to_host_tiles(self, source: str = "view"):
+        """[(vector_index int64, nm_index (V, G*N) int64, kept_values (V, G*N) float64)] per tile
+        (TileEncoding fields, pruning.py:261-273); ``source='image'`` decodes the operand image."""
+        tp, vi, nm, kv, _ = self.to_host_arrays(source)
         V, N, M = self.V, self.N, self.M
         out = []
         for t in range(self.T):
@@ -128,7 +156,6 @@ class DevicePack:
             w = k // M * N
             out.append((vi[tp[t]:tp[t + 1]].copy(), nm[b:b + V * w].reshape(V, w),
                         kv[b:b + V * w].reshape(V, w)))
-        del torch
         return out
 
     def replicate(self, device) -> "DevicePack":
@@ -176,12 +203,15 @@ def _empty_pack(vcfg: ValidatedConfig, device) -> DevicePack:
         kept=torch.empty(max(L, 1), dtype=torch.bfloat16, device=device))
 
 
-def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None):
+def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None,
+             saliency=None):
     """Fused GPU compressor (north-star subsystem 1): bf16 W (m x n, CUDA) + sigma -> DevicePack.
 
     ``sigma_o``: permutation of the m output channels; ``sigma_i``: optional per-tile gather
     orders (must be permutations of each tile's survivors, else InvariantViolation); default
-    ascending survivors.  Bit-exact with the reference's vector_prune -> nm_prune -> encode.
+    ascending survivors.  ``saliency``: optional external scores (m x n; numpy / SaliencyMatrix /
+    CUDA tensor, fp64 or fp32 -- the reference's ``encode --saliency`` path, cli.py:63-69,189-190);
+    default |W|.  Bit-exact with the reference's vector_prune -> nm_prune -> encode.
     """
     torch = _torch()
     _require_cuda(weights, "weights")
@@ -207,6 +237,19 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
                                            ctypes.byref(ws_bytes)), "compress_workspace")
     ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=dev)
     vmask = torch.empty(vcfg.num_tiles * n, dtype=torch.uint8, device=dev)
+    S = None
+    if saliency is not None:
+        from .model import SaliencyMatrix, as_values
+        from .pruning import _check_scores
+
+        raw = saliency.scores if isinstance(saliency, SaliencyMatrix) else saliency
+        if hasattr(raw, "is_cuda"):
+            S = raw.to(device=dev, dtype=torch.float64).contiguous()
+        else:
+            S = torch.as_tensor(np.ascontiguousarray(as_values(raw), dtype=np.float64)).to(dev)
+        if tuple(S.shape) != (m, n):
+            raise ShapeMismatch(f"saliency shape {tuple(S.shape)} does not match weights {(m, n)}")
+        _check_scores(saliency, S)
     sp = si = None
     if sigma_i is not None:
         sizes = [len(s) for s in sigma_i]
@@ -223,7 +266,8 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
         si = torch.as_tensor(flat.astype(np.int32)).to(dev)
     st = pack.struct()
     with torch.cuda.device(dev):
-        status = lib.hinm_compress_bf16(weights.data_ptr(), weights.stride(0), pack.sigma_o.data_ptr(),
+        status = lib.hinm_compress_bf16(weights.data_ptr(), weights.stride(0), _ptr(S),
+                                        0 if S is None else S.stride(0), pack.sigma_o.data_ptr(),
                                         _ptr(sp), _ptr(si), ctypes.byref(st), vmask.data_ptr(),
                                         ws.data_ptr(), ws_bytes.value, _stream_handle(dev))
     _lib.check(status, "compress")

@@ -55,3 +55,20 @@ def test_kernel_variant_matches_cross_check(env):
     r = subprocess.run([sys.executable, "-c", SNIPPET.format(root=ROOT)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"HINM_GATHER": "dbg_nomma"}, {"HINM_GW": "12"}, {"HINM_BN": "abc"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_product_library_rejects_unknown_knobs(env):
+    """Timing-only variants exist only in the experiments build; the product launcher refuses them
+    (and any malformed knob) instead of silently returning garbage or a default."""
+    snippet = (f"import sys; sys.path.insert(0, {ROOT!r})\n"
+               "import torch, paper_2407_20496_b200 as H\n"
+               "from paper_2407_20496_b200 import synth\n"
+               "W = torch.as_tensor(synth.randn_bf16((128, 256), 1)).cuda().to(torch.bfloat16)\n"
+               "p = H.compress(W, H.HiNMConfig(64, 2, 4, 0.5), list(range(128)))\n"
+               "X = torch.zeros(256, 64, dtype=torch.bfloat16, device='cuda')\n"
+               "try:\n    H.spmm(p, X)\nexcept ValueError:\n    print('rejected')\n")
+    r = subprocess.run([sys.executable, "-c", snippet], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=300)
+    assert r.stdout.strip().endswith("rejected"), r.stderr[-2000:]
