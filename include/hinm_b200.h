@@ -219,6 +219,20 @@ int hinm_last_launch_count(void);
  */
 int hinm_icp_costs(const double* vals, int V, int k, const int32_t* rem, const int32_t* samp,
                    int G, int M, int N, double* costs, void* stream);
+
+/*
+ * hinm_ocp_costs  <- _ocp_cost_matrix (the global output-channel assignment costs)  permutation.py:295-327
+ *   rem_cols / clu_cols: DEVICE P x n fp64 column scores of the partition remainders / sampled
+ *   clusters (tile_column_scores order); C: DEVICE P x P fp64,
+ *   C[i][j] = total - (sum of the k_groups largest of {gains of every remainder but i} U
+ *   gains(rem_cols[i] + clu_cols[j])).  One CTA per (i, j); the reference's per-pair lexsort +
+ *   np.partition become a keys-only block sort + a two-list merge over global prefix sums (the
+ *   retained sum differs from np.partition(...).sum() only in floating-point association).
+ *   n <= 16384.  Workspace from hinm_ocp_workspace.  Async.
+ */
+int hinm_ocp_workspace(int P, int n, int M, size_t* bytes);
+int hinm_ocp_costs(const double* rem_cols, const double* clu_cols, int P, int n, int M, int64_t k_groups,
+                   double total, double* C, void* workspace, size_t workspace_bytes, void* stream);
 int hinm_lex_assignment(const double* C, int n, int64_t* assignment);
 
 #ifdef __cplusplus

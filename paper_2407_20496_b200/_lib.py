@@ -84,6 +84,9 @@ _SIGNATURES = {
     "hinm_last_launch_count": ([], c_int),
     "hinm_icp_costs": ([c_vp, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "hinm_lex_assignment": ([c_vp, c_int, c_vp], c_int),
+    "hinm_ocp_workspace": ([c_int, c_int, c_int, ctypes.POINTER(c_size)], c_int),
+    "hinm_ocp_costs": ([c_vp, c_vp, c_int, c_int, c_int, c_i64, ctypes.c_double, c_vp, c_vp, c_size, c_vp],
+                       c_int),
 }
 EXPORTED = tuple(_SIGNATURES)
 

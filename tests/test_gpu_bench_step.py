@@ -8,6 +8,11 @@ units).  The packs are first checked bit-exactly against the oracle's compressor
 token columns of every output are compared with the oracle's float64 hinm_spmm +
 restore_row_order on the identical inputs (rtol 1e-2 / atol 1e-3, the north-star tolerance for bf16
 inputs with fp32 accumulation).
+
+Weights are N(0, 1/n) (the scale of a trained / initialised linear layer) so that outputs are O(1)
+and the absolute part of the tolerance means what it says: with N(0, 1) weights the down projection's
+outputs reach ~1e4 and single near-cancelling entries carry ~1e-2 of fp32 accumulation error --
+below the reference's own relative_error bound (checked too) but not an atol of 1e-3.
 """
 
 import numpy as np
@@ -37,7 +42,7 @@ def layers():
     cfg = H.HiNMConfig(V, 2, 4, 0.5)
     out = {}
     for i, (name, m, n) in enumerate(LAYERS):
-        Wh = synth.randn_bf16((m, n), 100 + i)
+        Wh = synth.bf16_round(synth.randn_bf16((m, n), 100 + i) / np.float32(np.sqrt(n)))
         so = synth.random_sigma_o(m, 200 + i)
         pack = H.compress(torch.as_tensor(Wh).cuda().to(torch.bfloat16), cfg, so)
         ref = O.compress(Wh.astype(np.float64), so, V, 2, 4, (m // V) * (n // 2))
@@ -67,3 +72,4 @@ def test_bench_step_matches_oracle(layers, tokens):
         ref = O.restore_row_order(O.hinm_spmm(tiles, inp, m, V, 2, 4), so)
         got = y[name].index_select(1, ci).float().cpu().numpy().astype(np.float64)
         np.testing.assert_allclose(got, ref, rtol=RTOL, atol=ATOL, err_msg=f"{name} @ {tokens} tokens")
+        assert O.relative_error(got, ref) < 1e-2

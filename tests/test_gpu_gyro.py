@@ -74,3 +74,23 @@ def test_icp_cost_kernel_bit_exact(V, M, N):
     ref = _ref_icp_costs(vals, rem, samp, N)
     got = P._IcpCostsGPU(vals, M, N)(np.array(rem), np.array(samp))
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("m,n,V,sv,samples", [(256, 128, 64, 0.5, 8), (512, 96, 32, 0.75, 4),
+                                              (384, 4096, 64, 0.5, 16), (128, 11008, 64, 0.5, 16)])
+def test_ocp_cost_kernel_matches_reference_loop(m, n, V, sv, samples):
+    """hinm_ocp_costs (one CTA per pair, sort + merge) vs the reference's per-pair lexsort +
+    np.partition (permutation.py:295-327): the same retained multiset, so equal up to floating-point
+    association (relative 1e-12); the assignment picked from either matrix is identical."""
+    rng = np.random.default_rng(m + n)
+    scores = np.abs(rng.standard_normal((m, n)))
+    scores[:, : n // 8] *= 1e-3                       # spread of magnitudes, as in real saliency
+    vcfg = H.validate_config(H.HiNMConfig(V, 2, 4, sv), (m, n))
+    tiles = P._tiles_of(rng.permutation(m), V)
+    rems, samp = P.sample_channels(tiles, samples, rng)
+    pool = np.concatenate(samp)
+    clusters = [np.sort(pool[q]) for q in P.balanced_kmeans(scores[pool], len(tiles), samples, rng)]
+    host = P._ocp_costs_host(scores, rems, clusters, vcfg)
+    dev = P._ocp_costs(scores, rems, clusters, vcfg)
+    np.testing.assert_allclose(dev, host, rtol=1e-12, atol=1e-9)
+    assert np.array_equal(P.hungarian(dev), P.hungarian(host))
