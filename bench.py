@@ -416,7 +416,7 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                   for _, m, n in layer_shapes())
     l2_bclk = None
     l2_tbs = (gathered + a_image) / (sum(per_kernel.values()) * 1e-3) / 1e12
-    ceiling = gather_ceiling()
+    ceiling = None if args.no_extras else gather_ceiling()
     binding = {"resource": "L2->SMEM gather fill (cp.async, 16 B per lane)",
                "achieved_tbs": round(l2_tbs, 2)}
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0

@@ -6,6 +6,9 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <mutex>
+#include <vector>
+
 #include "hinm_b200.h"
 
 #define HINM_CUDA_TRY(expr)                                                          \
@@ -21,6 +24,31 @@
 #define HINM_LAUNCH_CHECK() HINM_CUDA_TRY(cudaGetLastError())
 
 namespace hinm {
+
+// Dynamic shared-memory opt-in above 48 KB, cached per (kernel, device, bytes): the attribute call
+// costs host time on every launch otherwise (short kernels / per-call launch paths).
+inline cudaError_t smem_optin(const void* fn, int bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  struct Entry {
+    const void* fn;
+    int dev, bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : done)
+      if (e.fn == fn && e.dev == dev && e.bytes >= bytes) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    done.push_back({fn, dev, bytes});
+  }
+  return e;
+}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }

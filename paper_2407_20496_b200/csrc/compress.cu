@@ -260,6 +260,76 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const doubl
   }
 }
 
+// a4 (fast path, n <= 16384, fused): one CTA per tile sorts the tile's scores descending (keys
+// only: the order-preserving images of the scores, over the bits that differ inside the tile) and
+// writes, per M-chunk of the sorted scores, its gain (numpy summation order) and its last (smallest)
+// score -- everything the budget and the survivor pass need.  No column payload and no sorted copy
+// are written: survivors are recovered from the per-tile threshold score (k_survivors_thr).
+template <int NT, int ITEMS>
+__host__ __device__ constexpr size_t tile_gains_smem() {
+  return sizeof(typename cub::BlockRadixSort<uint64_t, NT, ITEMS>::TempStorage) > (size_t)NT * ITEMS * 8
+             ? sizeof(typename cub::BlockRadixSort<uint64_t, NT, ITEMS>::TempStorage)
+             : (size_t)NT * ITEMS * 8;
+}
+
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_tile_gains(const double* __restrict__ scores, int n, int M, int G,
+                                                  double* __restrict__ gains, double* __restrict__ cmin,
+                                                  unsigned long long* __restrict__ keybits) {
+  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS> BRS;
+  typedef cub::BlockReduce<uint64_t, NT> BR;
+  extern __shared__ __align__(16) uint8_t tg_smem[];
+  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(tg_smem);
+  double* vals = reinterpret_cast<double*>(tg_smem);
+  __shared__ typename BR::TempStorage red_tmp;
+  __shared__ uint64_t s_or, s_and;
+  const int t = blockIdx.x;
+  const double* row = scores + (int64_t)t * n;
+  uint64_t keys[ITEMS];
+  uint64_t lor = 0, land = ~0ull;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int j = threadIdx.x * ITEMS + i;
+    keys[i] = j < n ? ord_key(row[j]) : 0ull;
+    if (j < n) { lor |= keys[i]; land &= keys[i]; }
+  }
+  lor = BR(red_tmp).Reduce(lor, OrOp());
+  if (threadIdx.x == 0) s_or = lor;
+  __syncthreads();
+  land = BR(red_tmp).Reduce(land, AndOp());
+  if (threadIdx.x == 0) s_and = land;
+  __syncthreads();
+  const uint64_t diff = s_or ^ s_and;
+  if (diff) {
+    const int begin = __ffsll((long long)diff) - 1, end = 64 - __clzll((long long)diff);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (threadIdx.x * ITEMS + i >= n) keys[i] = s_and;  // padding: minimum partial key, after ties
+    BRS(tmp).SortDescending(keys, begin, end);
+    __syncthreads();                                   // temp storage is reused for the values
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) vals[threadIdx.x * ITEMS + i] = ord_value(keys[i]);
+  __syncthreads();
+  uint64_t kor = 0, kand = ~0ull;
+  for (int q = threadIdx.x; q < G; q += NT) {
+    auto get = [&](int64_t k) { return vals[(int64_t)q * M + k]; };
+    const double g = np_pairwise_sum(get, 0, M) + 0.0;
+    gains[(int64_t)t * G + q] = g;
+    cmin[(int64_t)t * G + q] = vals[(int64_t)q * M + M - 1];
+    const uint64_t k = gain_key(g);
+    kor |= k;
+    kand &= k;
+  }
+  kor = BR(red_tmp).Reduce(kor, OrOp());
+  __syncthreads();
+  kand = BR(red_tmp).Reduce(kand, AndOp());
+  if (threadIdx.x == 0) {  // one atomic pair per tile (not per warp)
+    atomicOr(keybits, (unsigned long long)kor);
+    atomicAnd(keybits + 1, (unsigned long long)kand);
+  }
+}
+
 // Tail of the budget selection once the threshold key xs (the G-th smallest (-gain) key) is
 // known: per-tile counts with ties ordered by (q, t), written as the tile_ptr prefix.
 template <int NT>
@@ -537,6 +607,53 @@ __global__ void __launch_bounds__(NT) k_survivors(const int32_t* __restrict__ or
     if (f) out[carry + ex] = j;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+// a6/a7 from the threshold: survivors of tile t = the k_t best columns by (score desc, column asc)
+// (lexsort, pruning.py:91-93, 163) = every column scoring above s* = the k_t-th largest score (the
+// last score of chunk k_t / M - 1) plus the lowest-indexed columns scoring exactly s*.  Emitted in
+// ascending column order (the default sigma_i, pruning.py:167-169) with the vector mask row.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_survivors_thr(const double* __restrict__ scores, int n, int M, int G,
+                                                      const double* __restrict__ cmin,
+                                                      const int32_t* __restrict__ tile_ptr,
+                                                      int32_t* __restrict__ surv, uint8_t* __restrict__ vmask) {
+  typedef cub::BlockScan<int, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ int64_t red;
+  __shared__ int carry_tie, carry_out;
+  const int t = blockIdx.x;
+  const int k = tile_ptr[t + 1] - tile_ptr[t];
+  const double* row = scores + (int64_t)t * n;
+  uint8_t* vm = vmask ? vmask + (int64_t)t * n : nullptr;
+  if (k == 0) {
+    if (vm)
+      for (int j = threadIdx.x; j < n; j += NT) vm[j] = 0;
+    return;
+  }
+  const double thr = cmin[(int64_t)t * G + k / M - 1];
+  int64_t above = 0;
+  for (int j = threadIdx.x; j < n; j += NT) above += row[j] > thr ? 1 : 0;
+  const int need = k - (int)block_sum64<NT>(above, &red);  // columns scoring exactly thr to keep
+  if (threadIdx.x == 0) { carry_tie = 0; carry_out = 0; }
+  __syncthreads();
+  int32_t* out = surv + tile_ptr[t];
+  for (int base = 0; base < n; base += NT) {
+    const int j = base + threadIdx.x;
+    const double v = j < n ? row[j] : 0.0;
+    const int tie = (j < n && v == thr) ? 1 : 0;
+    int tex, ttot;
+    BS(scan_tmp).ExclusiveSum(tie, tex, ttot);
+    __syncthreads();
+    const int keep = (j < n && (v > thr || (tie && carry_tie + tex < need))) ? 1 : 0;
+    int kex, ktot;
+    BS(scan_tmp).ExclusiveSum(keep, kex, ktot);
+    if (keep) out[carry_out + kex] = j;
+    if (vm && j < n) vm[j] = (uint8_t)keep;
+    __syncthreads();
+    if (threadIdx.x == 0) { carry_tie += ttot; carry_out += ktot; }
     __syncthreads();
   }
 }
@@ -1061,8 +1178,7 @@ int launch_tile_sort_items(const double* scores, int n, int T, double* sorted, i
   typedef cub::BlockRadixSort<uint64_t, NT, ITEMS, int32_t, 6> BRS;
   const size_t smem = sizeof(typename BRS::TempStorage);
   if (smem > 48 * 1024)
-    HINM_CUDA_TRY(cudaFuncSetAttribute(k_tile_sort<NT, ITEMS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HINM_CUDA_TRY(smem_optin((const void*)k_tile_sort<NT, ITEMS>, (int)smem));
   k_tile_sort<NT, ITEMS><<<T, NT, smem, stream>>>(scores, n, sorted, order);
   HINM_LAUNCH_CHECK();
   return HINM_OK;
@@ -1087,6 +1203,25 @@ int launch_tile_sort(const double* scores, int n, int T, double* sorted, int32_t
   if (n <= 8192) return launch_tile_sort_items<8>(scores, n, T, sorted, order, stream);
   if (n <= 12288) return launch_tile_sort_items<12>(scores, n, T, sorted, order, stream);
   return launch_tile_sort_items<16>(scores, n, T, sorted, order, stream);
+}
+
+template <int NT, int ITEMS>
+int launch_tile_gains_items(const double* scores, int n, int T, int M, int G, double* gains, double* cmin,
+                            unsigned long long* keybits, cudaStream_t stream) {
+  constexpr size_t smem = tile_gains_smem<NT, ITEMS>();
+  HINM_CUDA_TRY(smem_optin((const void*)k_tile_gains<NT, ITEMS>, (int)smem));
+  k_tile_gains<NT, ITEMS><<<T, NT, smem, stream>>>(scores, n, M, G, gains, cmin, keybits);
+  HINM_LAUNCH_CHECK();
+  return HINM_OK;
+}
+
+int launch_tile_gains(const double* scores, int n, int T, int M, int G, double* gains, double* cmin,
+                      unsigned long long* keybits, cudaStream_t stream) {
+  if (n <= 1024) return launch_tile_gains_items<256, 4>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  if (n <= 2048) return launch_tile_gains_items<256, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  if (n <= 4096) return launch_tile_gains_items<512, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  if (n <= 8192) return launch_tile_gains_items<1024, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  return launch_tile_gains_items<1024, 16>(scores, n, T, M, G, gains, cmin, keybits, stream);
 }
 
 int status_from_rank(int code, int mask_mode) {
@@ -1154,10 +1289,21 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   }
   HINM_LAUNCH_CHECK();
   const int64_t Tn = (int64_t)T * n;
-  k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
-  k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
-  HINM_LAUNCH_CHECK();
-  if (n <= 16384) {
+  if (n > 16384) {  // payload / offsets of the device-wide segmented sort
+    k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
+    k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
+    HINM_LAUNCH_CHECK();
+  }
+  uint32_t* ghist = (uint32_t*)(ws + L.ghist);
+  unsigned long long* keybits = (unsigned long long*)(ghist + 8 * 256);
+  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4 + 8, stream));
+  HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
+  const bool fused = n <= 16384 && G > 0;
+  double* cmin = sorted;  // fused path: per-chunk last score (T x G) in the sorted region
+  if (fused) {
+    int st2 = launch_tile_gains(scores, n, T, M, G, gains, cmin, keybits, stream);
+    if (st2) return st2;
+  } else if (n <= 16384) {
     // one CTA per tile, stable block radix sort (descending)
     int st2 = launch_tile_sort(scores, n, T, sorted, order, stream);
     if (st2) return st2;
@@ -1166,11 +1312,7 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     HINM_CUDA_TRY(cub::DeviceSegmentedRadixSort::SortPairsDescending(
         ws + L.cub, cb, scores, sorted, vals_in, order, Tn, T, offsets, offsets + 1, 0, 64, stream));
   }
-  uint32_t* ghist = (uint32_t*)(ws + L.ghist);
-  unsigned long long* keybits = (unsigned long long*)(ghist + 8 * 256);
-  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4 + 8, stream));
-  HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
-  if (G > 0) {
+  if (G > 0 && !fused) {
     k_gains<<<(unsigned)ceil_div((int64_t)T * G, 256), 256, 0, stream>>>(sorted, n, M, G, T, gains,
                                                                          keybits);
     HINM_LAUNCH_CHECK();
@@ -1198,10 +1340,14 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
                                                 args, 0, stream));
     }
   }
+  if (fused) {
+    k_survivors_thr<1024><<<T, 1024, 0, stream>>>(scores, n, M, G, cmin, tile_ptr, surv, vector_mask);
+    HINM_LAUNCH_CHECK();
+    return HINM_OK;
+  }
   const size_t smem = (size_t)n;
   if (smem > 48 * 1024)
-    HINM_CUDA_TRY(cudaFuncSetAttribute(k_survivors<1024>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HINM_CUDA_TRY(smem_optin((const void*)k_survivors<1024>, (int)smem));
   k_survivors<1024><<<T, 1024, smem, stream>>>(order, n, tile_ptr, surv, vector_mask);
   HINM_LAUNCH_CHECK();
   return HINM_OK;
@@ -1242,8 +1388,7 @@ extern "C" int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const do
     goto done;
   }
   if (vsmem > 48 * 1024 &&
-      cudaFuncSetAttribute(k_validate_sigma<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)vsmem) != cudaSuccess) {
+      smem_optin((const void*)k_validate_sigma<256>, (int)vsmem) != cudaSuccess) {
     status = HINM_ERR_CUDA;
     goto done;
   }
@@ -1353,8 +1498,7 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
     HINM_LAUNCH_CHECK();
     if (fsmem > 48 * 1024)
-      HINM_CUDA_TRY(cudaFuncSetAttribute(k_select_pack<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fsmem));
+      HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
     k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
         W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
         p->a_vals, (uint32_t*)p->a_meta, p->gidx);
@@ -1362,8 +1506,7 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
   } else if (fast) {
     constexpr int R = 4;
     if (rsmem > 48 * 1024)
-      HINM_CUDA_TRY(cudaFuncSetAttribute(k_nm_select_rows<256, R>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+      HINM_CUDA_TRY(smem_optin((const void*)k_nm_select_rows<256, R>, (int)rsmem));
     dim3 grid((unsigned)ceil_div(p->V, R), p->T);
     k_nm_select_rows<256, R><<<grid, 256, rsmem, stream>>>(W, ldw, sigma_o, sp, si, p->n, p->V, p->N,
                                                            p->M, p->nm_pos, p->kept_bf16);

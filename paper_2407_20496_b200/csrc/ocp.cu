@@ -299,8 +299,7 @@ extern "C" int hinm_ocp_costs(const double* rem_cols, const double* clu_cols, in
     constexpr int NT = decltype(nt)::value, IT = decltype(items)::value;
     const size_t dyn = sort_bytes<NT, IT>();
     if (dyn > 48 * 1024)
-      HINM_CUDA_TRY(cudaFuncSetAttribute(k_row_gains<NT, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dyn));
+      HINM_CUDA_TRY(smem_optin((const void*)k_row_gains<NT, IT>, (int)dyn));
     k_row_gains<NT, IT><<<P, NT, dyn, st>>>(rem_cols, nullptr, n, M, 0, rg);
     HINM_LAUNCH_CHECK();
     return HINM_OK;
@@ -332,8 +331,7 @@ extern "C" int hinm_ocp_costs(const double* rem_cols, const double* clu_cols, in
     constexpr int NT = decltype(nt)::value, IT = decltype(items)::value;
     const size_t dyn = sort_bytes<NT, IT>() + (size_t)(G + 1) * 8;
     if (dyn > 48 * 1024)
-      HINM_CUDA_TRY(cudaFuncSetAttribute(k_ocp_pairs<NT, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dyn));
+      HINM_CUDA_TRY(smem_optin((const void*)k_ocp_pairs<NT, IT>, (int)dyn));
     k_ocp_pairs<NT, IT><<<(unsigned)((int64_t)P * P), NT, dyn, st>>>(rem_cols, clu_cols, n, M, k_groups,
                                                                       total, o, C);
     HINM_LAUNCH_CHECK();

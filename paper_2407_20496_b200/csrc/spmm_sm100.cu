@@ -745,27 +745,7 @@ int sm_count(int dev) {
   return g_sms[dev];
 }
 
-struct SmemOptIn {
-  const void* fn;
-  int dev;
-  int bytes;
-};
-std::mutex g_optin_mu;
-std::vector<SmemOptIn> g_optin;
-
-cudaError_t ensure_smem(const void* fn, int dev, int bytes) {
-  {
-    std::lock_guard<std::mutex> lk(g_optin_mu);
-    for (const SmemOptIn& o : g_optin)
-      if (o.fn == fn && o.dev == dev && o.bytes >= bytes) return cudaSuccess;
-  }
-  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) {
-    std::lock_guard<std::mutex> lk(g_optin_mu);
-    g_optin.push_back({fn, dev, bytes});
-  }
-  return e;
-}
+cudaError_t ensure_smem(const void* fn, int /*dev*/, int bytes) { return hinm::smem_optin(fn, bytes); }
 
 }  // namespace
 

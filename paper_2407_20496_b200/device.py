@@ -203,6 +203,40 @@ def _empty_pack(vcfg: ValidatedConfig, device) -> DevicePack:
         kept=torch.empty(max(L, 1), dtype=torch.bfloat16, device=device))
 
 
+_WS_CACHE: dict = {}
+_WS_LOCK = __import__("threading").Lock()
+
+
+def _workspace(dev, stream: int, nbytes: int):
+    """Compressor workspace reused per (device, stream): calls on one stream are ordered, so a
+    cached buffer is never live in two calls at once; a few entries are kept (LRU)."""
+    torch = _torch()
+    key = (dev.index, stream)
+    with _WS_LOCK:
+        ws = _WS_CACHE.pop(key, None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        _WS_CACHE[key] = ws
+        while len(_WS_CACHE) > 4:
+            _WS_CACHE.pop(next(iter(_WS_CACHE)))
+    return ws
+
+
+def _carve(dev, parts):
+    """One device allocation for all of a pack's arrays (256-byte aligned views)."""
+    torch = _torch()
+    offs, total = [], 0
+    for _, dtype, count in parts:
+        offs.append(total)
+        total += -(-max(count, 1) * torch.empty(0, dtype=dtype).element_size() // 256) * 256
+    buf = torch.empty(total, dtype=torch.uint8, device=dev)
+    out = {}
+    for (name, dtype, count), o in zip(parts, offs):
+        size = max(count, 1) * torch.empty(0, dtype=dtype).element_size()
+        out[name] = buf[o:o + size].view(dtype)
+    return out
+
+
 def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None,
              saliency=None):
     """Fused GPU compressor (north-star subsystem 1): bf16 W (m x n, CUDA) + sigma -> DevicePack.
@@ -223,20 +257,34 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
     from .pruning import check_sigma_o
 
     check_sigma_o(sigma_o, m)
-    so = torch.from_numpy(np.ascontiguousarray(sigma_o, dtype=np.int32)).to(dev) if not (
-        hasattr(sigma_o, "is_cuda")) else sigma_o.to(device=dev, dtype=torch.int32)
-    pack = _empty_pack(vcfg, dev)
-    pack.sigma_o = so.contiguous()
     if build_operand_image is None:
         build_operand_image = spmm_supported(vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group)
-    if build_operand_image:
-        _alloc_operand_image(pack)
     lib = _lib.load()
+    V, N, M, K, T = vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group, vcfg.total_keep, vcfg.num_tiles
+    L = V * K // M * N
+    parts = [("sigma_o", torch.int32, m), ("tile_ptr", torch.int32, T + 1), ("vec_idx", torch.int32, K),
+             ("nm_pos", torch.uint8, L), ("kept", torch.bfloat16, L), ("vector_mask", torch.uint8, T * n)]
+    kc = mc = 0
+    if build_operand_image:
+        kc_, mc_, ac_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(lib.hinm_pack_capacity(m, n, V, K, ctypes.byref(kc_), ctypes.byref(mc_),
+                                          ctypes.byref(ac_)), "pack_capacity")
+        kc, mc = kc_.value, mc_.value
+        parts += [("tile_kofs", torch.int32, T + 1), ("tile_eofs", torch.int32, T + 1),
+                  ("gidx", torch.int32, kc), ("a_vals", torch.bfloat16, ac_.value), ("a_meta", torch.int32, mc)]
+    a = _carve(dev, parts)
+    if hasattr(sigma_o, "is_cuda"):
+        a["sigma_o"].copy_(sigma_o.reshape(-1))
+    else:
+        # pinned staging: a pageable copy would synchronize the stream (and the compressions before)
+        host = torch.from_numpy(np.ascontiguousarray(sigma_o, dtype=np.int32)).pin_memory()
+        a["sigma_o"].copy_(host, non_blocking=True)
+    vmask = a.pop("vector_mask")
+    pack = DevicePack(m, n, V, N, M, K, vcfg.config, kpad_cap=kc, meta_cap=mc, **a)
     ws_bytes = ctypes.c_size_t()
-    _lib.check(lib.hinm_compress_workspace(m, n, vcfg.vector_size, vcfg.nm_group,
-                                           ctypes.byref(ws_bytes)), "compress_workspace")
-    ws = torch.empty(max(ws_bytes.value, 1), dtype=torch.uint8, device=dev)
-    vmask = torch.empty(vcfg.num_tiles * n, dtype=torch.uint8, device=dev)
+    _lib.check(lib.hinm_compress_workspace(m, n, V, M, ctypes.byref(ws_bytes)), "compress_workspace")
+    stream = _stream_handle(dev)
+    ws = _workspace(dev, stream, ws_bytes.value)
     S = None
     if saliency is not None:
         from .model import SaliencyMatrix, as_values
@@ -269,7 +317,7 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
         status = lib.hinm_compress_bf16(weights.data_ptr(), weights.stride(0), _ptr(S),
                                         0 if S is None else S.stride(0), pack.sigma_o.data_ptr(),
                                         _ptr(sp), _ptr(si), ctypes.byref(st), vmask.data_ptr(),
-                                        ws.data_ptr(), ws_bytes.value, _stream_handle(dev))
+                                        ws.data_ptr(), ws_bytes.value, stream)
     _lib.check(status, "compress")
     pack.vector_mask = vmask.view(vcfg.num_tiles, n)
     return pack

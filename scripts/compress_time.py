@@ -1,26 +1,51 @@
-"""Time the fused GPU compressor (hinm_compress_bf16) on the LLaMA FFN shapes."""
-import json, os, sys, time
+"""Time the fused GPU compressor (hinm_compress_bf16 through device.compress) on the LLaMA FFN shapes.
+
+    python scripts/compress_time.py [reps]
+
+Per shape: host wall of one call (min), stream time of one call (CUDA events around it, median) and
+the per-call stream time of `reps` back-to-back calls (host enqueue overlapped with the GPU), with the
+achieved fraction of HBM bandwidth for the algorithmic bytes (2mn + m k + m k / 8 + 4 T k + 4m).
+"""
+import json, os, statistics, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2407_20496_b200 as H
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6543.4
 out = {}
 for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
     g = torch.Generator(device="cuda").manual_seed(1)
     W = torch.randn(m, n, generator=g, device="cuda").to(torch.bfloat16)
     so = np.random.default_rng(2).permutation(m)
     cfg = H.HiNMConfig(64, 2, 4, 0.5)
-    H.compress(W, cfg, so)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
+    for _ in range(3):
         H.compress(W, cfg, so)
+    torch.cuda.synchronize()
+    wall, stream = [], []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        e0.record()
+        H.compress(W, cfg, so)
+        e1.record()
+        torch.cuda.synchronize()
+        wall.append(time.perf_counter() - t0)
+        stream.append(e0.elapsed_time(e1))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        H.compress(W, cfg, so)
+    e1.record()
+    torch.cuda.synchronize()
+    b2b = e0.elapsed_time(e1) / reps
     kbar = n // 2
     alg = 2 * m * n + m * kbar + m * kbar // 8 + 4 * (m // 64) * kbar + 4 * m
-    best = min(ts)
-    out[name] = {"ms": round(best * 1e3, 3), "algorithmic_bytes": alg, "gbs": round(alg / best / 1e9, 1)}
+    st = statistics.median(stream)
+    out[name] = {"wall_ms": round(min(wall) * 1e3, 3), "stream_ms": round(st, 3), "b2b_ms": round(b2b, 3),
+                 "algorithmic_bytes": alg, "gbs_stream": round(alg / st / 1e6, 1),
+                 "hbm_frac_stream": round(alg / st / 1e6 / peak, 4),
+                 "hbm_frac_b2b": round(alg / b2b / 1e6 / peak, 4)}
 print(json.dumps(out))
