@@ -265,33 +265,58 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const doubl
 // writes, per M-chunk of the sorted scores, its gain (numpy summation order) and its last (smallest)
 // score -- everything the budget and the survivor pass need.  No column payload and no sorted copy
 // are written: survivors are recovered from the per-tile threshold score (k_survivors_thr).
+// Radix digit width of the tile sorts: cub's rank counters take 2^(bits-1) x NT x 4 bytes of shared
+// memory, so 1024-thread CTAs use 5-bit digits and smaller CTAs 6-bit digits.
+template <int NT>
+constexpr int tile_radix_bits() { return NT >= 1024 ? 5 : 6; }
+
 template <int NT, int ITEMS>
-__host__ __device__ constexpr size_t tile_gains_smem() {
-  return sizeof(typename cub::BlockRadixSort<uint64_t, NT, ITEMS>::TempStorage) > (size_t)NT * ITEMS * 8
-             ? sizeof(typename cub::BlockRadixSort<uint64_t, NT, ITEMS>::TempStorage)
-             : (size_t)NT * ITEMS * 8;
+struct TileSort {
+  typedef cub::BlockRadixSort<uint32_t, NT, ITEMS, cub::NullType, tile_radix_bits<NT>()> S32;
+  typedef cub::BlockRadixSort<uint32_t, NT, ITEMS, uint32_t, tile_radix_bits<NT>()> P32;
+  static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+  static constexpr size_t bytes =
+      cmax(cmax(sizeof(typename S32::TempStorage), sizeof(typename P32::TempStorage)), (size_t)NT * ITEMS * 8);
+};
+
+template <int NT, int ITEMS>
+__host__ __device__ constexpr size_t tile_gains_smem() { return TileSort<NT, ITEMS>::bytes; }
+
+// numpy's sum of M consecutive values (pairwise_sum: a plain loop below 8 terms)
+template <class Get>
+__device__ __forceinline__ double chunk_sum(const Get& get, int M) {
+  if (M < 8) {
+    double acc = 0.0;
+    for (int k = 0; k < M; ++k) acc = acc + get(k);
+    return acc;
+  }
+  return np_pairwise_sum(get, 0, M);
 }
 
+// a4 (fast path, n <= 16384, fused): one CTA per tile sorts the tile's scores descending (keys
+// only: the order-preserving images of the scores, over the bits that differ inside the tile --
+// as 32-bit keys when those bits span <= 32, the common case: column sums of bf16 magnitudes share
+// their sign / top exponent bits and end in zero mantissa bits) and writes, per M-chunk of the
+// sorted scores, its gain (numpy summation order) and its last (smallest) score -- everything the
+// budget and the survivor pass need.  No column payload and no sorted copy are written: survivors
+// are recovered from the per-tile threshold score (k_survivors_thr).
 template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_tile_gains(const double* __restrict__ scores, int n, int M, int G,
                                                   double* __restrict__ gains, double* __restrict__ cmin,
                                                   unsigned long long* __restrict__ keybits) {
-  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS> BRS;
+  typedef TileSort<NT, ITEMS> TS;
   typedef cub::BlockReduce<uint64_t, NT> BR;
   extern __shared__ __align__(16) uint8_t tg_smem[];
-  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(tg_smem);
   double* vals = reinterpret_cast<double*>(tg_smem);
   __shared__ typename BR::TempStorage red_tmp;
   __shared__ uint64_t s_or, s_and;
   const int t = blockIdx.x;
   const double* row = scores + (int64_t)t * n;
-  uint64_t keys[ITEMS];
   uint64_t lor = 0, land = ~0ull;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int j = threadIdx.x * ITEMS + i;
-    keys[i] = j < n ? ord_key(row[j]) : 0ull;
-    if (j < n) { lor |= keys[i]; land &= keys[i]; }
+  for (int j = threadIdx.x; j < n; j += NT) {
+    const uint64_t k = ord_key(row[j]);
+    lor |= k;
+    land &= k;
   }
   lor = BR(red_tmp).Reduce(lor, OrOp());
   if (threadIdx.x == 0) s_or = lor;
@@ -299,24 +324,52 @@ __global__ void __launch_bounds__(NT) k_tile_gains(const double* __restrict__ sc
   land = BR(red_tmp).Reduce(land, AndOp());
   if (threadIdx.x == 0) s_and = land;
   __syncthreads();
-  const uint64_t diff = s_or ^ s_and;
-  if (diff) {
-    const int begin = __ffsll((long long)diff) - 1, end = 64 - __clzll((long long)diff);
+  const uint64_t diff = s_or ^ s_and, base = s_and;
+  const int begin = diff ? __ffsll((long long)diff) - 1 : 0;
+  const int width = diff ? 64 - __clzll((long long)diff) - begin : 0;
+  if (width <= 32) {
+    // key = the varying field; padding 0 sorts after every real key (stable: ties keep order)
+    uint32_t keys[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int j = threadIdx.x * ITEMS + i;
+      keys[i] = j < n ? (uint32_t)((ord_key(row[j]) ^ base) >> begin) : 0u;
+    }
+    if (width) {
+      typename TS::S32::TempStorage& tmp = *reinterpret_cast<typename TS::S32::TempStorage*>(tg_smem);
+      TS::S32(tmp).SortDescending(keys, 0, width);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) vals[threadIdx.x * ITEMS + i] = ord_value(base | ((uint64_t)keys[i] << begin));
+  } else {
+    // wider fields: two stable 32-bit passes, least significant first (low 32 bits of the field,
+    // then the rest), each carrying the other half as payload
+    uint32_t lo[ITEMS], hi[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int j = threadIdx.x * ITEMS + i;
+      const uint64_t f = j < n ? (ord_key(row[j]) ^ base) >> begin : 0ull;
+      lo[i] = (uint32_t)f;
+      hi[i] = (uint32_t)(f >> 32);
+    }
+    typename TS::P32::TempStorage& tmp = *reinterpret_cast<typename TS::P32::TempStorage*>(tg_smem);
+    TS::P32(tmp).SortDescending(lo, hi, 0, 32);
+    __syncthreads();
+    TS::P32(tmp).SortDescending(hi, lo, 0, width - 32);
+    __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
-      if (threadIdx.x * ITEMS + i >= n) keys[i] = s_and;  // padding: minimum partial key, after ties
-    BRS(tmp).SortDescending(keys, begin, end);
-    __syncthreads();                                   // temp storage is reused for the values
+      vals[threadIdx.x * ITEMS + i] = ord_value(base | ((((uint64_t)hi[i] << 32) | lo[i]) << begin));
   }
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) vals[threadIdx.x * ITEMS + i] = ord_value(keys[i]);
   __syncthreads();
   uint64_t kor = 0, kand = ~0ull;
   for (int q = threadIdx.x; q < G; q += NT) {
-    auto get = [&](int64_t k) { return vals[(int64_t)q * M + k]; };
-    const double g = np_pairwise_sum(get, 0, M) + 0.0;
+    const double* c = vals + (int64_t)q * M;
+    auto get = [&](int64_t k) { return c[k]; };
+    const double g = chunk_sum(get, M) + 0.0;
     gains[(int64_t)t * G + q] = g;
-    cmin[(int64_t)t * G + q] = vals[(int64_t)q * M + M - 1];
+    cmin[(int64_t)t * G + q] = c[M - 1];
     const uint64_t k = gain_key(g);
     kor |= k;
     kand &= k;
@@ -489,8 +542,13 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
 }
 
 
-// a5, multi-CTA: the same radix select with the key histogram split over the whole grid
-// (cooperative launch, one grid-wide barrier per 8-bit digit).
+// a5, multi-CTA: radix select of the G-th smallest budget key over the whole grid (cooperative
+// launch).  11-bit digits over only the key bits that differ between some keys (OR / AND words
+// from the gains pass): ~3 passes of one CTA-wide shared histogram each and one grid barrier per
+// pass; then one warp per tile finds its bounds around the threshold key and block 0 applies the
+// (q, t) tie order (budget_tail).
+constexpr int BUDGET_BITS = 11, BUDGET_BINS = 1 << BUDGET_BITS, BUDGET_MAX_PASSES = 6;
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ gains, int T, int G,
                                                     int64_t total_groups, int M,
@@ -502,72 +560,68 @@ __global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ g
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   constexpr int NW = NT / 32;
-  __shared__ uint32_t hist[NW][256];
+  constexpr int PER = BUDGET_BINS / NT;  // bins per thread in the bucket search
+  typedef cub::BlockScan<uint32_t, NT> BS;
+  __shared__ uint32_t hist[BUDGET_BINS];
+  __shared__ typename BS::TempStorage scan_tmp;
   __shared__ uint64_t s_prefix;
   __shared__ int64_t s_k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t total = (int64_t)T * G;
-  // bytes on which all keys agree need no pass: they are taken from the AND of the keys
+  // bits on which all keys agree need no pass: they are taken from the AND of the keys
   const uint64_t kor = __ldcg(keybits), kand = __ldcg(keybits + 1), diff = kor ^ kand;
-  const int top = diff ? (63 - __clzll((long long)diff)) / 8 * 8 : -8;
-  const int bottom = diff ? (__ffsll((long long)diff) - 1) / 8 * 8 : 0;
-  const uint64_t above = top >= 56 ? 0ull : ~0ull << (top + 8);
+  const int top = diff ? 63 - __clzll((long long)diff) : -1;      // highest differing bit
+  const int low = diff ? __ffsll((long long)diff) - 1 : 0;         // lowest differing bit
+  const uint64_t above = top >= 63 ? 0ull : ~0ull << (top + 1);
   uint64_t prefix = kand & above, pmask = above;
   int64_t k = total_groups;
   int pass = 0;
-  for (int shift = top; shift >= bottom; shift -= 8, ++pass) {
-    for (int i = threadIdx.x; i < NW * 256; i += NT) (&hist[0][0])[i] = 0;
+  for (int hi = top; hi >= low; hi -= BUDGET_BITS, ++pass) {
+    const int shift = hi - BUDGET_BITS + 1 > low ? hi - BUDGET_BITS + 1 : low;  // digit = bits [shift, hi]
+    const int nbits = hi - shift + 1;
+    const uint32_t dmask = (1u << nbits) - 1u;
+    for (int i = threadIdx.x; i < BUDGET_BINS; i += NT) hist[i] = 0;
     __syncthreads();
     for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
       const int64_t i = i0 + threadIdx.x;
       const uint64_t d = i < total ? gain_key(gains[i]) : 0;
       const bool cand = i < total && (d & pmask) == prefix;
-      const uint32_t bin = (uint32_t)(d >> shift) & 255u;
+      const uint32_t bin = (uint32_t)(d >> shift) & dmask;
       const uint32_t act = __ballot_sync(0xffffffffu, cand);
       if (cand) {
         const uint32_t peers = __match_any_sync(act, bin);
-        if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[warp][bin], (uint32_t)__popc(peers));
+        if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
       }
     }
     __syncthreads();
-    for (int bn = threadIdx.x; bn < 256; bn += NT) {
-      uint32_t v = 0;
-      for (int w = 0; w < NW; ++w) v += hist[w][bn];
-      if (v) atomicAdd(ghist + pass * 256 + bn, v);
-    }
+    uint32_t* gh = ghist + pass * BUDGET_BINS;
+    for (int bn = threadIdx.x; bn < BUDGET_BINS; bn += NT)
+      if (hist[bn]) atomicAdd(gh + bn, hist[bn]);
     grid.sync();
-    if (warp == 0) {
-      uint32_t c[8];
-      uint32_t sum = 0;
+    // every CTA finds the bin holding rank k (bins PER per thread, one block scan)
+    uint32_t c[PER], sum = 0;
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        c[b] = __ldcg(ghist + pass * 256 + lane * 8 + b);
-        sum += c[b];
-      }
-      uint32_t incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t excl = incl - sum;
-      const bool mine = (int64_t)excl < k && k <= (int64_t)incl;
-      const uint32_t who = __ballot_sync(0xffffffffu, mine);
-      if (lane == __ffs(who) - 1) {
-        int64_t before = excl;
-        int b = 0;
-        while (before + c[b] < k) { before += c[b]; ++b; }
-        s_prefix = prefix | ((uint64_t)(lane * 8 + b) << shift);
-        s_k = k - before;
-      }
+    for (int b2 = 0; b2 < PER; ++b2) {
+      c[b2] = __ldcg(gh + threadIdx.x * PER + b2);
+      sum += c[b2];
+    }
+    uint32_t excl;
+    BS(scan_tmp).ExclusiveSum(sum, excl);
+    if ((int64_t)excl < k && k <= (int64_t)excl + sum) {
+      int64_t before = excl;
+      int b2 = 0;
+      while (before + c[b2] < k) { before += c[b2]; ++b2; }
+      s_prefix = prefix | ((uint64_t)(threadIdx.x * PER + b2) << shift);
+      s_k = k - before;
     }
     __syncthreads();
     prefix = s_prefix;
     k = s_k;
-    pmask |= (uint64_t)255 << shift;
+    pmask |= (uint64_t)dmask << shift;
     __syncthreads();
+    if (shift == low) break;
   }
-  prefix |= kand & ~pmask;  // constant low bytes
+  prefix |= kand & ~pmask;  // constant low bits
   for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {  // one warp per tile
     const double* row = gains + (int64_t)t * G;
     const int a = row_bound_warp(row, G, prefix, false), b = row_bound_warp(row, G, prefix, true);
@@ -1049,10 +1103,12 @@ __global__ void __launch_bounds__(NT) k_select_pack(
   const size_t row_bytes = ((size_t)n * 2 + 15) & ~size_t(15);
   int32_t* s_idx = reinterpret_cast<int32_t*>(sp_smem);
   uint8_t* s_rows = sp_smem + idx_bytes;
+  const int nr = min(R, V - r0);
+  // all R weight rows of the CTA at once (one HBM pass over W overall), overlapped with the index load
   const bool vec_rows = (ldw & 7) == 0 && (n & 7) == 0 && ((uintptr_t)W & 15) == 0;
-  auto fetch_row = [&](int rr) {
+  for (int rr = 0; rr < nr; ++rr) {
     const uint16_t* wrow = W + (int64_t)sigma_o[(int64_t)t * V + r0 + rr] * ldw;
-    uint16_t* dst = reinterpret_cast<uint16_t*>(s_rows + (rr & 1) * row_bytes);
+    uint16_t* dst = reinterpret_cast<uint16_t*>(s_rows + rr * row_bytes);
     if (vec_rows) {
       for (int i = threadIdx.x; i < n / 8; i += NT) {
         const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + 8 * i);
@@ -1061,39 +1117,36 @@ __global__ void __launch_bounds__(NT) k_select_pack(
     } else {
       for (int i = threadIdx.x; i < n; i += NT) dst[i] = wrow[i];
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  fetch_row(0);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // group column indices (padding entries repeat a valid column: their values are ignored)
   for (int i = threadIdx.x; i < kp; i += NT) s_idx[i] = sig_idx[b + (i < k ? i : k - 1)];
   if (r0 == 0)
     for (int i = threadIdx.x; i < kp; i += NT) gidx[kofs + i] = sig_idx[b + (i < k ? i : k - 1)];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   const int64_t ref_base = (int64_t)V * (b / 4) * 2;
   const int nch = kp / 16;        // 16-K chunks with values
   const int nch_meta = nblk * 8;  // chunks covered by metadata blocks (>= nch)
   uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
-  for (int rr = 0; rr < R; ++rr) {
-    const int r = r0 + rr;
-    if (rr + 1 < R) {
-      fetch_row(rr + 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const uint16_t* row = reinterpret_cast<const uint16_t*>(s_rows + (rr & 1) * row_bytes);
-    const int64_t rbase = ref_base + (int64_t)r * G * 2;
-    const int m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
-    for (int ch = threadIdx.x; ch < nch_meta; ch += NT) {
-      const int g0 = ch * 4;
+  for (int ch = threadIdx.x; ch < nch_meta; ch += NT) {
+    const int g0 = ch * 4;
+    // the chunk's 4 groups of column indices, loaded once for all R rows
+    int4 c4[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) c4[c] = g0 + c < G ? reinterpret_cast<const int4*>(s_idx)[g0 + c] : make_int4(0, 0, 0, 0);
+    const int eb = g0 >> 5, w = (g0 >> 3) & 3, k1 = (g0 >> 2) & 1;
+#pragma unroll 2
+    for (int rr = 0; rr < nr; ++rr) {
+      const int r = r0 + rr;
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(s_rows + rr * row_bytes);
+      const int64_t rbase = ref_base + (int64_t)r * G * 2;
       uint32_t pos[4], val[4];
       uint32_t bits = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int g = g0 + c;
-        if (g < G) {
-          const int4 c4 = reinterpret_cast<const int4*>(s_idx)[g];
-          top2_of_4(row[c4.x], row[c4.y], row[c4.z], row[c4.w], pos[c], val[c]);
+        if (g0 + c < G) {
+          top2_of_4(row[c4[c].x], row[c4[c].y], row[c4[c].z], row[c4[c].w], pos[c], val[c]);
         } else {
           pos[c] = 0x100u;  // positions {0, 1}, zero values
           val[c] = 0u;
@@ -1115,10 +1168,9 @@ __global__ void __launch_bounds__(NT) k_select_pack(
       if (ch < nch)  // operand image: 8 compressed values = one 16-byte core-matrix row
         *reinterpret_cast<uint4*>(a_vals + aval_offset(kofs, V, r, 2 * g0)) =
             make_uint4(val[0], val[1], val[2], val[3]);
-      const int eb = g0 >> 5, w = (g0 >> 3) & 3, k1 = (g0 >> 2) & 1;
+      const int m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
       meta16[(((int64_t)eb * V + m0 + 8 * k1 + 16 * m2) * 4 + w) * 2 + m1] = (uint16_t)bits;
     }
-    __syncthreads();  // row buffer (rr & 1) is refilled by the next iteration's fetch
   }
 }
 
@@ -1163,7 +1215,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->hi = take(4 * T);
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
   L->err = take(16);
-  L->ghist = take(8 * 256 * 4 + 16);  // radix histograms + key OR / AND words
+  L->ghist = take(BUDGET_MAX_PASSES * BUDGET_BINS * 4 + 16);  // radix histograms + key OR / AND words
   size_t cb = 0;
   int st = cub_sort_bytes((int)T, n, &cb);
   if (st) return st;
@@ -1220,8 +1272,11 @@ int launch_tile_gains(const double* scores, int n, int T, int M, int G, double* 
   if (n <= 1024) return launch_tile_gains_items<256, 4>(scores, n, T, M, G, gains, cmin, keybits, stream);
   if (n <= 2048) return launch_tile_gains_items<256, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
   if (n <= 4096) return launch_tile_gains_items<512, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  if (n <= 8192) return launch_tile_gains_items<1024, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  return launch_tile_gains_items<1024, 16>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  // 512-thread CTAs keep the keys (and the payload of the wide-field path) in registers: 1024
+  // threads would cap every thread at 64 registers and spill
+  if (n <= 8192) return launch_tile_gains_items<512, 16>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  if (n <= 11264) return launch_tile_gains_items<512, 22>(scores, n, T, M, G, gains, cmin, keybits, stream);
+  return launch_tile_gains_items<512, 32>(scores, n, T, M, G, gains, cmin, keybits, stream);
 }
 
 int status_from_rank(int code, int mask_mode) {
@@ -1295,8 +1350,8 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     HINM_LAUNCH_CHECK();
   }
   uint32_t* ghist = (uint32_t*)(ws + L.ghist);
-  unsigned long long* keybits = (unsigned long long*)(ghist + 8 * 256);
-  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, 8 * 256 * 4 + 8, stream));
+  unsigned long long* keybits = (unsigned long long*)(ghist + BUDGET_MAX_PASSES * BUDGET_BINS);
+  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, BUDGET_MAX_PASSES * BUDGET_BINS * 4 + 8, stream));
   HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
   const bool fused = n <= 16384 && G > 0;
   double* cmin = sorted;  // fused path: per-chunk last score (T x G) in the sorted region
@@ -1328,7 +1383,8 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_budget_coop<1024>, 1024, 0);
     }
     const int64_t total = (int64_t)T * G;
-    int nblk = (int)std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, ceil_div(total, 4096)));
+    // one 1024-key slice per CTA and pass (every SM busy on the LLaMA shapes), at most one wave
+    int nblk = (int)std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, ceil_div(total, 1024)));
     if (per_sm < 1 || nblk < 2) {
       k_budget_radix<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, lo_s, hi_s, tile_ptr);
       HINM_LAUNCH_CHECK();
@@ -1487,7 +1543,7 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
   }
   // fused select + operand-image pack (2:4, V in {32, 64, 128}, operand image requested)
   const size_t kp_cap = (size_t)round_up(p->n, 64);
-  const size_t fsmem = ((kp_cap * 4 + 15) & ~size_t(15)) + 2 * (((size_t)p->n * 2 + 15) & ~size_t(15));
+  const size_t fsmem = ((kp_cap * 4 + 15) & ~size_t(15)) + 2 * (((size_t)p->n * 2 + 15) & ~size_t(15));  // R = 2
   const bool fused = fast && p->a_vals && p->N == 2 && p->M == 4 &&
                      (p->V == 32 || p->V == 64 || p->V == 128) && fsmem <= 200 * 1024 &&
                      p->tile_kofs && p->tile_eofs && p->gidx && p->a_meta;
@@ -1497,12 +1553,20 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
     k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
     HINM_LAUNCH_CHECK();
-    if (fsmem > 48 * 1024)
-      HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
-    k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
-        W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
-        p->a_vals, (uint32_t*)p->a_meta, p->gidx);
-    HINM_LAUNCH_CHECK();
+    // as many staged weight rows per CTA as fit (8 -> one index load serves 8 rows)
+    const size_t rowb = ((size_t)p->n * 2 + 15) & ~size_t(15);
+    const size_t idxb = (kp_cap * 4 + 15) & ~size_t(15);
+    auto go = [&](auto kern, int R) -> int {
+      const size_t smem = idxb + (size_t)R * rowb;
+      HINM_CUDA_TRY(smem_optin((const void*)kern, (int)smem));
+      kern<<<dim3((unsigned)ceil_div(p->V, R), p->T), 128, smem, stream>>>(
+          W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
+          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+      HINM_LAUNCH_CHECK();
+      return HINM_OK;
+    };
+    int rc = idxb + 8 * rowb <= 200 * 1024 ? go(k_select_pack<128, 8>, 8) : go(k_select_pack<128, 2>, 2);
+    if (rc) return rc;
   } else if (fast) {
     constexpr int R = 4;
     if (rsmem > 48 * 1024)

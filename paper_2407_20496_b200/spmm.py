@@ -222,25 +222,15 @@ def tile_shuffle_check(enc: HiNMEncoding, inputs, rng, trials: int = 50,
 
 @dataclass(frozen=True)
 class LayerChain:
-    """Encoded layers; layer l consumes layer l-1's output rows in their sigma_o order."""
+    """Encoded layers; layer l consumes layer l-1's output rows in their sigma_o order
+    (spmm.py:38-47)."""
 
     layers: tuple
 
-
-def _identity_permute(W, cfg, saliency=None):
-    """The reference's ``no_perm_prune`` (permutation.py:644-646): identity sigma_o, ascending
-    survivors as sigma_i -- the GPU compressor's own-sigma_i mode."""
-    from .model import GyroPermutation, MaskPair, ensure_validated
-    from .pruning import magnitude_saliency, nm_prune, survivors_per_tile, vector_prune
-
-    m, n = as_values(W).shape
-    vcfg = ensure_validated(cfg, (m, n))
-    S = magnitude_saliency(W) if saliency is None else saliency
-    so = np.arange(m, dtype=np.int64)
-    vm = vector_prune(S, vcfg.config, so)
-    sigma = GyroPermutation(sigma_o=so, sigma_i=tuple(survivors_per_tile(vm)))
-    return sigma, MaskPair(vector_mask=np.asarray(vm), element_mask=np.asarray(
-        nm_prune(S, vm, vcfg.config, sigma))), None
+    @property
+    def final_sigma_o(self) -> np.ndarray:
+        """Row order of the chain's output: the last layer's sigma_o (spmm.py:45-47)."""
+        return self.layers[-1].sigma_o
 
 
 def build_layer_chain(weight_matrices, cfgs, saliencies=None, permute=None) -> LayerChain:
@@ -249,13 +239,13 @@ def build_layer_chain(weight_matrices, cfgs, saliencies=None, permute=None) -> L
     layer consumes its predecessor's output rows directly (no restore between layers).
 
     ``permute(W, cfg, saliency=...) -> (GyroPermutation, MaskPair, report)`` is the permutation
-    search; the reference uses ``gyro_permute`` (permutation.py:549), which is outside this GPU
-    path -- pass it in to reproduce the reference exactly.  The default is the
-    identity pipeline (``no_perm_prune``).
+    search; the default is the reference's ``gyro_permute`` (permutation.py:549; this package's
+    GPU implementation, bit-identical), ``no_perm_prune`` gives the identity pipeline.
     """
+    from .permutation import gyro_permute
     from .pruning import encode
 
-    permute = permute or _identity_permute
+    permute = permute or gyro_permute
     if not isinstance(cfgs, (list, tuple)):
         cfgs = [cfgs] * len(weight_matrices)
     if saliencies is None:

@@ -32,7 +32,7 @@ def nxt():
 
 
 def test_build_layer_chain_matches_reference(nxt):
-    chain = H.build_layer_chain([nxt["chain_W1"], nxt["chain_W2"]], CFG)
+    chain = H.build_layer_chain([nxt["chain_W1"], nxt["chain_W2"]], CFG, permute=H.no_perm_prune)
     for l, enc in enumerate(chain.layers):
         assert np.array_equal(enc.sigma_o, nxt[f"chain_l{l}_sigma_o"])
         for t, tile in enumerate(enc.tiles):
@@ -41,8 +41,27 @@ def test_build_layer_chain_matches_reference(nxt):
             assert np.array_equal(tile.kept_values, nxt[f"chain_l{l}_t{t}_kv"])
 
 
+def test_build_layer_chain_default_gyro_matches_reference():
+    """The reference's own build_layer_chain with its default search (gyro_permute, reduced budgets):
+    identical sigma_o, encodings and chain output (tests/golden/make_golden_chain.py)."""
+    z = np.load(os.path.join(GOLD, "chain_gyro.npz"))
+    cfg = H.HiNMConfig(vector_size=32, nm_keep=2, nm_group=4, vector_sparsity=0.5, ocp_max_iters=3,
+                       icp_max_iters=3, seed=5)
+    W1 = synth.randn_bf16((128, 96), 51).astype(np.float64)
+    W2 = synth.randn_bf16((64, 128), 52).astype(np.float64)
+    X = synth.randn_bf16((96, 16), 53).astype(np.float64)
+    chain = H.build_layer_chain([W1, W2], cfg)
+    for l, enc in enumerate(chain.layers):
+        assert np.array_equal(enc.sigma_o, z[f"l{l}_sigma_o"])
+        assert np.array_equal(np.concatenate([t.vector_index for t in enc.tiles]), z[f"l{l}_vi"])
+        assert np.array_equal(np.concatenate([t.nm_index.ravel() for t in enc.tiles]), z[f"l{l}_nm"])
+        assert np.array_equal(np.concatenate([t.kept_values.ravel() for t in enc.tiles]), z[f"l{l}_kv"])
+    assert np.array_equal(chain.final_sigma_o, z["final_sigma_o"])
+    assert O.relative_error(H.compose_layers(chain, X), z["Y"]) < 1e-2
+
+
 def test_compose_layers_matches_reference(nxt):
-    chain = H.build_layer_chain([nxt["chain_W1"], nxt["chain_W2"]], CFG)
+    chain = H.build_layer_chain([nxt["chain_W1"], nxt["chain_W2"]], CFG, permute=H.no_perm_prune)
     Y = H.compose_layers(chain, nxt["chain_X"])
     # two bf16 layers (bf16 activations between them, fp32 accumulation) vs float64
     assert O.relative_error(Y, nxt["chain_Y"]) < 1e-2
