@@ -231,6 +231,14 @@ int hinm_icp_costs(const double* vals, int V, int k, const int32_t* rem, const i
  *   n <= 16384.  Workspace from hinm_ocp_workspace.  Async.
  */
 int hinm_ocp_workspace(int P, int n, int M, size_t* bytes);
+
+/*
+ * hinm_sq_dists   <- the balanced k-means distances of the OCP sampling  permutation.py:102-145
+ *   out[p][c] = ((points[p] - centroids[c]) ** 2).sum() in numpy's pairwise summation order
+ *   (bit-identical).  points: DEVICE P x F, centroids: DEVICE C x F, out: DEVICE P x C fp64.  Async.
+ */
+int hinm_sq_dists(const double* points, int P, const double* centroids, int C, int F, double* out,
+                  void* stream);
 int hinm_ocp_costs(const double* rem_cols, const double* clu_cols, int P, int n, int M, int64_t k_groups,
                    double total, double* C, void* workspace, size_t workspace_bytes, void* stream);
 int hinm_lex_assignment(const double* C, int n, int64_t* assignment);

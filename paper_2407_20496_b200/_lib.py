@@ -85,6 +85,7 @@ _SIGNATURES = {
     "hinm_icp_costs": ([c_vp, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "hinm_lex_assignment": ([c_vp, c_int, c_vp], c_int),
     "hinm_ocp_workspace": ([c_int, c_int, c_int, ctypes.POINTER(c_size)], c_int),
+    "hinm_sq_dists": ([c_vp, c_int, c_vp, c_int, c_int, c_vp, c_vp], c_int),
     "hinm_ocp_costs": ([c_vp, c_vp, c_int, c_int, c_int, c_i64, ctypes.c_double, c_vp, c_vp, c_size, c_vp],
                        c_int),
 }

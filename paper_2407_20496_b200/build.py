@@ -28,7 +28,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libhinm_b200.so")
 EXP_LIB = os.path.join(ROOT, "scripts", "libhinm_b200_exp.so")
 SOURCES = ["compress.cu", "spmm_sm100.cu", "spmm_simt.cu", "chain_host.cu", "capi.cu",
-           "icp.cu", "assignment.cu", "unpack.cu", "ocp.cu"]
+           "icp.cu", "assignment.cu", "unpack.cu", "ocp.cu", "kmeans.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]

@@ -47,6 +47,29 @@ def test_gyro_permute_matches_reference(g, name):
     assert rep.to_dict() == REPORTS[name]["report"]
 
 
+def test_balanced_kmeans_matches_reference(g):
+    """k-means++ seeding + capacitated Lloyd rounds with the distances on the GPU (hinm_sq_dists,
+    numpy pairwise order): the reference's labels bit-for-bit."""
+    for t in range(6):
+        k = t + 2
+        pts = g[f"km_pts{t}"]
+        groups = P.balanced_kmeans(pts, k, 6, np.random.default_rng(t))
+        lab = np.empty(pts.shape[0], dtype=np.int64)
+        for c, idx in enumerate(groups):
+            lab[idx] = c
+        assert np.array_equal(lab, g[f"km_lab{t}"]), t
+
+
+def test_sq_dists_bit_exact_with_numpy():
+    rng = np.random.default_rng(4)
+    for P_, C, F in ((37, 5, 1), (64, 7, 3), (50, 9, 129), (33, 4, 4096), (12, 3, 11008)):
+        pts = rng.standard_normal((P_, F)) * rng.choice([1.0, 1e-3, 1e3], size=(P_, F))
+        cents = rng.standard_normal((C, F))
+        ref = ((pts[:, None, :] - cents[None, :, :]) ** 2).sum(axis=-1)
+        assert np.array_equal(P._Dists(pts)(cents), ref), (P_, C, F)
+        assert np.array_equal(P._Dists(pts)(cents[0])[:, 0], ((pts - cents[0]) ** 2).sum(axis=1))
+
+
 def _ref_icp_costs(vals, rem, samp, N):
     G = len(samp)
     C = np.empty((G, G))

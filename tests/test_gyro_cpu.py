@@ -1,6 +1,6 @@
-"""Gyro-permutation search, host parts (no GPU): the native lexicographic assignment and the
-balanced k-means against the reference's outputs (tests/golden/gyro.npz, generator
-tests/golden/make_golden_gyro.py)."""
+"""Gyro-permutation search, host parts (no GPU): the native lexicographic assignment against the
+reference's outputs (tests/golden/gyro.npz, generator tests/golden/make_golden_gyro.py); the
+balanced k-means (GPU distances) is checked in test_gpu_gyro.py."""
 
 import os
 
@@ -41,17 +41,6 @@ def test_hungarian_is_optimal_and_lexicographic():
     D = rng.integers(0, 3, (6, 6)).astype(float)
     best = min(permutations(range(6)), key=lambda p: (sum(D[i, p[i]] for i in range(6)), p))
     assert tuple(P.hungarian(D)) == best
-
-
-def test_balanced_kmeans_matches_reference(g):
-    for t in range(6):
-        k = t + 2
-        pts = g[f"km_pts{t}"]
-        groups = P.balanced_kmeans(pts, k, 6, np.random.default_rng(t))
-        lab = np.empty(pts.shape[0], dtype=np.int64)
-        for c, idx in enumerate(groups):
-            lab[idx] = c
-        assert np.array_equal(lab, g[f"km_lab{t}"]), t
 
 
 def test_sample_channels_sizes():
