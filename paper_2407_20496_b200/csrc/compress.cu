@@ -1087,42 +1087,27 @@ __device__ __forceinline__ void top2_of_4(uint16_t v0, uint16_t v1, uint16_t v2,
   vals = (uint32_t)k0 | ((uint32_t)k1 << 16);
 }
 
-// Shared-memory bytes of k_select_pack for R staged rows: indices, weight rows, and the staged
-// operand image of those rows (values: kp/2 per row; metadata: one 16-bit half-word per chunk and row).
-__host__ __device__ inline size_t select_pack_smem(int n, int kp_cap, int R) {
-  const size_t idx = ((size_t)kp_cap * 4 + 15) & ~size_t(15);
-  const size_t row = ((size_t)n * 2 + 15) & ~size_t(15);
-  const size_t av = (size_t)R * kp_cap;            // kp_cap / 2 values x 2 bytes per row
-  const size_t meta = ((size_t)R * (kp_cap / 16 + 8) * 2 + 15) & ~size_t(15);
-  return idx + (size_t)R * row + av + meta;
-}
-
 template <int NT, int R>
 __global__ void __launch_bounds__(NT) k_select_pack(
     const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
-    const int32_t* __restrict__ sig_ptr, const int32_t* __restrict__ sig_idx, int n, int V, int kp_cap,
+    const int32_t* __restrict__ sig_ptr, const int32_t* __restrict__ sig_idx, int n, int V,
     const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
     uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
     uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
-  constexpr int RPG = R < 4 ? R : 4;  // rows served by one index load
   extern __shared__ __align__(16) uint8_t sp_smem[];
   const int t = blockIdx.y, r0 = blockIdx.x * R;
   const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
   const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
   const int eofs = eofs_g[t], nblk = eofs_g[t + 1] - eofs;
   if (kp == 0) return;
-  const size_t idx_bytes = ((size_t)kp_cap * 4 + 15) & ~size_t(15);
+  const size_t idx_bytes = ((size_t)kp * 4 + 15) & ~size_t(15);
   const size_t row_bytes = ((size_t)n * 2 + 15) & ~size_t(15);
   int32_t* s_idx = reinterpret_cast<int32_t*>(sp_smem);
   uint8_t* s_rows = sp_smem + idx_bytes;
-  uint16_t* s_av = reinterpret_cast<uint16_t*>(s_rows + (size_t)R * row_bytes);   // [step][rr][16]
-  uint16_t* s_meta = s_av + (size_t)R * kp_cap / 2;                              // [chunk][rr]
-  const int nr = min(R, V - r0);
-  // all R weight rows of the CTA at once (one HBM pass over W overall), overlapped with the index load
   const bool vec_rows = (ldw & 7) == 0 && (n & 7) == 0 && ((uintptr_t)W & 15) == 0;
-  for (int rr = 0; rr < nr; ++rr) {
+  auto fetch_row = [&](int rr) {
     const uint16_t* wrow = W + (int64_t)sigma_o[(int64_t)t * V + r0 + rr] * ldw;
-    uint16_t* dst = reinterpret_cast<uint16_t*>(s_rows + rr * row_bytes);
+    uint16_t* dst = reinterpret_cast<uint16_t*>(s_rows + (rr & 1) * row_bytes);
     if (vec_rows) {
       for (int i = threadIdx.x; i < n / 8; i += NT) {
         const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + 8 * i);
@@ -1131,40 +1116,39 @@ __global__ void __launch_bounds__(NT) k_select_pack(
     } else {
       for (int i = threadIdx.x; i < n; i += NT) dst[i] = wrow[i];
     }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch_row(0);
   // group column indices (padding entries repeat a valid column: their values are ignored)
   for (int i = threadIdx.x; i < kp; i += NT) s_idx[i] = sig_idx[b + (i < k ? i : k - 1)];
   if (r0 == 0)
     for (int i = threadIdx.x; i < kp; i += NT) gidx[kofs + i] = sig_idx[b + (i < k ? i : k - 1)];
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
   const int64_t ref_base = (int64_t)V * (b / 4) * 2;
   const int nch = kp / 16;        // 16-K chunks with values
   const int nch_meta = nblk * 8;  // chunks covered by metadata blocks (>= nch)
-  const int ngrp = (nr + RPG - 1) / RPG;
-  // item = (row group, chunk): lanes walk consecutive chunks of one row group, so the reference-view
-  // stores (row-major per row) coalesce; the operand image goes to shared memory first
-  for (int it = threadIdx.x; it < nch_meta * ngrp; it += NT) {
-    const int ch = it % nch_meta, rg = it / nch_meta;
-    const int g0 = ch * 4;
-    int4 c4[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      c4[c] = g0 + c < G ? reinterpret_cast<const int4*>(s_idx)[g0 + c] : make_int4(0, 0, 0, 0);
-#pragma unroll
-    for (int q = 0; q < RPG; ++q) {
-      const int rr = rg * RPG + q;
-      if (rr >= nr) break;
-      const int r = r0 + rr;
-      const uint16_t* row = reinterpret_cast<const uint16_t*>(s_rows + rr * row_bytes);
-      const int64_t rbase = ref_base + (int64_t)r * G * 2;
+  uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
+  for (int rr = 0; rr < R; ++rr) {
+    const int r = r0 + rr;
+    if (rr + 1 < R) {
+      fetch_row(rr + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(s_rows + (rr & 1) * row_bytes);
+    const int64_t rbase = ref_base + (int64_t)r * G * 2;
+    const int m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
+    for (int ch = threadIdx.x; ch < nch_meta; ch += NT) {
+      const int g0 = ch * 4;
       uint32_t pos[4], val[4];
       uint32_t bits = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if (g0 + c < G) {
-          top2_of_4(row[c4[c].x], row[c4[c].y], row[c4[c].z], row[c4[c].w], pos[c], val[c]);
+        const int g = g0 + c;
+        if (g < G) {
+          const int4 c4 = reinterpret_cast<const int4*>(s_idx)[g];
+          top2_of_4(row[c4.x], row[c4.y], row[c4.z], row[c4.w], pos[c], val[c]);
         } else {
           pos[c] = 0x100u;  // positions {0, 1}, zero values
           val[c] = 0u;
@@ -1183,31 +1167,13 @@ __global__ void __launch_bounds__(NT) k_select_pack(
           }
         }
       }
-      if (ch < nch)  // 8 compressed values: step ch / 2, half (ch & 1) of the 16-value core-matrix row pair
-        *reinterpret_cast<uint4*>(s_av + ((size_t)(ch >> 1) * R + rr) * 16 + (ch & 1) * 8) =
+      if (ch < nch)  // operand image: 8 compressed values = one 16-byte core-matrix row
+        *reinterpret_cast<uint4*>(a_vals + aval_offset(kofs, V, r, 2 * g0)) =
             make_uint4(val[0], val[1], val[2], val[3]);
-      s_meta[(size_t)ch * R + rr] = (uint16_t)bits;
+      const int eb = g0 >> 5, w = (g0 >> 3) & 3, k1 = (g0 >> 2) & 1;
+      meta16[(((int64_t)eb * V + m0 + 8 * k1 + 16 * m2) * 4 + w) * 2 + m1] = (uint16_t)bits;
     }
-  }
-  __syncthreads();
-  // operand image out, coalesced: per MMA step the CTA's rows are 2 runs of R x 16 bytes
-  // (core-matrix halves h = 0, 1; row r at (r >> 3) * 128 + h * 64 + (r & 7) * 8 values)
-  const int nsteps = kp / 32;
-  for (int u = threadIdx.x; u < nsteps * 2 * nr; u += NT) {
-    const int s2 = u / (2 * nr), q = u % (2 * nr), h = q / nr, rr = q % nr;
-    const int r = r0 + rr;
-    const int64_t dst = ((int64_t)kofs >> 1) * V + (int64_t)(s2 >> 1) * 32 * V + (int64_t)(s2 & 1) * 16 * V +
-                        (r >> 3) * 128 + h * 64 + (r & 7) * 8;
-    *reinterpret_cast<uint4*>(a_vals + dst) =
-        *reinterpret_cast<const uint4*>(s_av + ((size_t)s2 * R + rr) * 16 + h * 8);
-  }
-  // metadata out: word w fastest, then the row, so consecutive threads write neighbouring half-words
-  uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
-  for (int it = threadIdx.x; it < nch_meta * nr; it += NT) {
-    const int w = it & 3, rest = it >> 2, rr = rest % nr, rest2 = rest / nr, k1 = rest2 & 1, eb = rest2 >> 1;
-    const int ch = eb * 8 + w * 2 + k1;
-    const int r = r0 + rr, m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
-    meta16[(((int64_t)eb * V + m0 + 8 * k1 + 16 * m2) * 4 + w) * 2 + m1] = s_meta[(size_t)ch * R + rr];
+    __syncthreads();  // row buffer (rr & 1) is refilled by the next iteration's fetch
   }
 }
 
@@ -1580,7 +1546,7 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
   }
   // fused select + operand-image pack (2:4, V in {32, 64, 128}, operand image requested)
   const size_t kp_cap = (size_t)round_up(p->n, 64);
-  const size_t fsmem = select_pack_smem(p->n, (int)kp_cap, 4);
+  const size_t fsmem = ((kp_cap * 4 + 15) & ~size_t(15)) + 2 * (((size_t)p->n * 2 + 15) & ~size_t(15));
   const bool fused = fast && p->a_vals && p->N == 2 && p->M == 4 &&
                      (p->V == 32 || p->V == 64 || p->V == 128) && fsmem <= 200 * 1024 &&
                      p->tile_kofs && p->tile_eofs && p->gidx && p->a_meta;
@@ -1590,20 +1556,15 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
     k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
     HINM_LAUNCH_CHECK();
-    // as many staged weight rows per CTA as fit (8: one core-matrix row group, 2 x 4-row index reuse)
-    auto go = [&](auto kern, int R) -> int {
-      const size_t smem = select_pack_smem(p->n, (int)kp_cap, R);
-      HINM_CUDA_TRY(smem_optin((const void*)kern, (int)smem));
-      kern<<<dim3((unsigned)ceil_div(p->V, R), p->T), 256, smem, stream>>>(
-          W, ldw, sigma_o, sp, si, p->n, p->V, (int)kp_cap, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
-          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
-      HINM_LAUNCH_CHECK();
-      return HINM_OK;
-    };
-    static const int env_r = getenv("HINM_SP_R") ? atoi(getenv("HINM_SP_R")) : 0;  // 4 | 8 (tuning)
-    const bool r8 = env_r == 8 || (env_r != 4 && select_pack_smem(p->n, (int)kp_cap, 8) <= 120 * 1024);
-    int rc = r8 && select_pack_smem(p->n, (int)kp_cap, 8) <= 200 * 1024 ? go(k_select_pack<256, 8>, 8)
-                                                                        : go(k_select_pack<256, 4>, 4);
+    // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory (measured: 4 rows
+    // staged at once with a shared index load, or the operand image staged and written coalesced,
+    // were both slower on the LLaMA shapes -- 84-101 us vs 56-60 us per layer)
+    HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
+    k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
+        W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
+        p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+    HINM_LAUNCH_CHECK();
+    int rc = HINM_OK;
     if (rc) return rc;
   } else if (fast) {
     constexpr int R = 4;

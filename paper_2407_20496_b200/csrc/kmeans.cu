@@ -21,8 +21,8 @@ __global__ void k_sq_dists(const double* __restrict__ pts, int P, const double* 
   const double* a = pts + p * F;
   const double* b = cents + c * F;
   auto get = [&](int64_t f) {
-    const double d = a[f] - b[f];
-    return d * d;
+    const double d = __dsub_rn(a[f], b[f]);
+    return __dmul_rn(d, d);  // rounded before the add: no FMA contraction (numpy squares, then sums)
   };
   out[i] = np_pairwise_sum(get, 0, F);
 }
