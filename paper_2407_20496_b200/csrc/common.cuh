@@ -100,6 +100,45 @@ __device__ double np_pairwise_sum(const Get& get, int64_t lo, int64_t n) {
   return np_pairwise_sum(get, lo, half) + np_pairwise_sum(get, lo + half, n - half);
 }
 
+// The same summation tree without recursion (long operands: every recursion level costs a device
+// stack frame and the default 1 KB stack overflows around n ~ 10^4).  Explicit post-order walk.
+template <class Get>
+__device__ double np_pairwise_sum_iter(const Get& get, int64_t lo, int64_t n) {
+  struct Frame {
+    int64_t lo, n;
+    double left;
+    int stage;  // 0: left child pending, 1: right child pending
+  };
+  Frame st[40];
+  int sp = 0;
+  st[0] = {lo, n, 0.0, 0};
+  double ret = 0.0;
+  while (true) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {  // leaf: the unrolled 8-accumulator block (or a plain loop below 8)
+      ret = np_pairwise_sum(get, f.lo, f.n);
+    } else if (f.stage == 0) {
+      int64_t half = f.n / 2;
+      half -= half % 8;
+      f.stage = 1;
+      st[++sp] = {f.lo, half, 0.0, 0};
+      continue;
+    } else {
+      int64_t half = f.n / 2;
+      half -= half % 8;
+      if (f.stage == 1) {  // left done (in ret): descend right
+        f.left = ret;
+        f.stage = 2;
+        st[++sp] = {f.lo + half, f.n - half, 0.0, 0};
+        continue;
+      }
+      ret = f.left + ret;  // both children done
+    }
+    if (sp == 0) return ret;
+    --sp;
+  }
+}
+
 // Device error word: lowest (tile, rank) wins, mirroring the reference's per-tile check order.
 __device__ __forceinline__ void report_error(int* err, int tile, int rank_code) {
   atomicMin(err, tile * 16 + rank_code);

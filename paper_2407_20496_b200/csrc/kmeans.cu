@@ -24,7 +24,7 @@ __global__ void k_sq_dists(const double* __restrict__ pts, int P, const double* 
     const double d = __dsub_rn(a[f], b[f]);
     return __dmul_rn(d, d);  // rounded before the add: no FMA contraction (numpy squares, then sums)
   };
-  out[i] = np_pairwise_sum(get, 0, F);
+  out[i] = np_pairwise_sum_iter(get, 0, F);
 }
 
 }  // namespace

@@ -459,33 +459,19 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     constexpr int RPW = KS / GW;  // K-rows per warp per stage
     static_assert(KS % GW == 0 && GW >= 8 && RPW <= 32, "gather producers: GW | KS, GW >= 8");
     const int dt = gridDim.x % T, dnb = gridDim.x / T;
-    // prefetch cursor: unit (pt, pnb) with running index pu, stage ps, kp of the unit.  The tile
-    // offsets of the FOLLOWING unit are loaded one unit ahead (ahead_k0 / ahead_k1): a dependent
-    // global load at the unit switch would stall the warp for the L1tex queue's full latency under
-    // gather load (~4k cycles per unit boundary, measured as the up-vs-down projection gap).
+    // prefetch cursor: unit (pt, pnb) with running index pu, stage ps, kp of the unit
     int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pkp = 0;
-    int ahead_k0 = 0, ahead_k1 = 0;
-    auto step_unit = [&]() {
-      pu += gridDim.x;
-      pt += dt;
-      pnb += dnb;
-      if (pt >= T) { pt -= T; ++pnb; }
-    };
-    auto load_ahead = [&]() {  // offsets of the unit after (pu, pt): consumed one unit later
-      int t2 = pt + dt;
-      if (t2 >= T) t2 -= T;
-      ahead_k0 = __ldg(p.tile_kofs + t2);
-      ahead_k1 = __ldg(p.tile_kofs + t2 + 1);
-    };
-    auto next_unit = [&]() {  // advance to the next unit with work (blocking loads: start / empty tiles)
+    auto next_unit = [&]() {  // advance to the next unit with work
       while (pu < p.units) {
         pk0 = __ldg(p.tile_kofs + pt);
         pkp = __ldg(p.tile_kofs + pt + 1) - pk0;
         if (pkp > 0) break;
-        step_unit();
+        pu += gridDim.x;
+        pt += dt;
+        pnb += dnb;
+        if (pt >= T) { pt -= T; ++pnb; }
       }
       ps = 0;
-      load_ahead();
     };
     next_unit();
     const uint32_t ldx2 = p.xpitch;  // row pitch in bytes (host: < 2^32)
@@ -505,11 +491,11 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         // raw row index: it is consumed PF stages later, so the load never stalls the warp here
         r_row[j] = lane < RPW && gw + lane * GW < n ? (uint32_t)__ldg(gi + gw + lane * GW) : 0u;
         if (++ps * KS >= pkp) {
-          step_unit();
-          pk0 = ahead_k0;                 // loaded a whole unit ago
-          pkp = ahead_k1 - ahead_k0;
-          ps = 0;
-          if (pkp > 0) load_ahead(); else next_unit();  // empty tile: skip with blocking loads
+          pu += gridDim.x;
+          pt += dt;
+          pnb += dnb;
+          if (pt >= T) { pt -= T; ++pnb; }
+          next_unit();
         }
       }
     };
