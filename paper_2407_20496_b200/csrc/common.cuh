@@ -100,39 +100,65 @@ __device__ double np_pairwise_sum(const Get& get, int64_t lo, int64_t n) {
   return np_pairwise_sum(get, lo, half) + np_pairwise_sum(get, lo + half, n - half);
 }
 
-// The same summation tree without recursion (long operands: every recursion level costs a device
-// stack frame and the default 1 KB stack overflows around n ~ 10^4).  Explicit post-order walk.
+// numpy's pairwise block for n <= 128 (no recursion): 8 accumulators, then the remainder.
+template <class Get>
+__device__ __forceinline__ double np_pairwise_leaf(const Get& get, int64_t lo, int64_t n) {
+  if (n < 8) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc = acc + get(lo + i);
+    return acc;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+  int64_t i = 8;
+  const int64_t stop = n - (n % 8);
+  for (; i < stop; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = r[j] + get(lo + i + j);
+  }
+  double acc = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) acc = acc + get(lo + i);
+  return acc;
+}
+
+// The same summation tree without recursion, for long operands (every recursion level costs a
+// device-stack frame; the default 1 KB stack overflows around n ~ 10^4): an explicit post-order
+// walk with a small frame stack (16 levels: n up to 128 * 2^15).
 template <class Get>
 __device__ double np_pairwise_sum_iter(const Get& get, int64_t lo, int64_t n) {
-  struct Frame {
-    int64_t lo, n;
-    double left;
-    int stage;  // 0: left child pending, 1: right child pending
-  };
-  Frame st[40];
+  constexpr int DEPTH = 16;
+  int32_t f_lo[DEPTH], f_n[DEPTH];
+  double f_left[DEPTH];
+  uint8_t f_stage[DEPTH];
   int sp = 0;
-  st[0] = {lo, n, 0.0, 0};
+  f_lo[0] = (int32_t)lo;
+  f_n[0] = (int32_t)n;
+  f_stage[0] = 0;
   double ret = 0.0;
   while (true) {
-    Frame& f = st[sp];
-    if (f.n <= 128) {  // leaf: the unrolled 8-accumulator block (or a plain loop below 8)
-      ret = np_pairwise_sum(get, f.lo, f.n);
-    } else if (f.stage == 0) {
-      int64_t half = f.n / 2;
-      half -= half % 8;
-      f.stage = 1;
-      st[++sp] = {f.lo, half, 0.0, 0};
+    const int32_t cn = f_n[sp];
+    int32_t half = cn / 2;
+    half -= half % 8;
+    if (cn <= 128) {
+      ret = np_pairwise_leaf(get, f_lo[sp], cn);
+    } else if (f_stage[sp] == 0) {
+      f_stage[sp] = 1;
+      f_lo[sp + 1] = f_lo[sp];
+      f_n[sp + 1] = half;
+      f_stage[sp + 1] = 0;
+      ++sp;
+      continue;
+    } else if (f_stage[sp] == 1) {  // left done (in ret): descend right
+      f_left[sp] = ret;
+      f_stage[sp] = 2;
+      f_lo[sp + 1] = f_lo[sp] + half;
+      f_n[sp + 1] = cn - half;
+      f_stage[sp + 1] = 0;
+      ++sp;
       continue;
     } else {
-      int64_t half = f.n / 2;
-      half -= half % 8;
-      if (f.stage == 1) {  // left done (in ret): descend right
-        f.left = ret;
-        f.stage = 2;
-        st[++sp] = {f.lo + half, f.n - half, 0.0, 0};
-        continue;
-      }
-      ret = f.left + ret;  // both children done
+      ret = f_left[sp] + ret;  // both children done
     }
     if (sp == 0) return ret;
     --sp;

@@ -33,6 +33,7 @@ __global__ void k_sq_dists(const double* __restrict__ pts, int P, const double* 
 extern "C" int hinm_sq_dists(const double* points, int P, const double* centroids, int C, int F, double* out,
                              void* stream) {
   if (!points || !centroids || !out || P < 0 || C < 0 || F < 1) return HINM_ERR_VALUE;
+  if (F > (128 << 15)) return HINM_ERR_UNSUPPORTED;  // depth of the summation-tree walk
   const int64_t n = (int64_t)P * C;
   if (n == 0) return HINM_OK;
   hinm::k_sq_dists<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(points, P, centroids, C, F,
