@@ -1,10 +1,11 @@
-"""Small end-to-end run for compute-sanitizer (memcheck / synccheck / racecheck): compressor +
-tcgen05 SpMM at V in {32, 64, 128}, both output orders, ragged tokens, an empty tile."""
+"""Small end-to-end run for compute-sanitizer (memcheck / synccheck / racecheck): compressor (|W| and
+external-saliency paths) + tcgen05 SpMM at V in {32, 64, 128}, both output orders, ragged tokens,
+the operand-image decoder, and the gyro search's GPU kernels (OCP costs, k-means distances, ICP)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2407_20496_b200 as H
-from paper_2407_20496_b200 import synth
+from paper_2407_20496_b200 import permutation as P, synth
 
 for V, m, n, B in ((64, 256, 512, 264), (32, 128, 256, 64), (128, 256, 384, 136)):
     W = torch.as_tensor(synth.randn_bf16((m, n), V)).to("cuda", torch.bfloat16)
@@ -16,4 +17,11 @@ for V, m, n, B in ((64, 256, 512, 264), (32, 128, 256, 64), (128, 256, 384, 136)
         torch.cuda.synchronize()
         err = (Y.float() - R).abs().max().item() / max(R.abs().max().item(), 1e-30)
         assert err < 1e-2, err
+    assert np.array_equal(pack.to_host_arrays("image")[2], pack.to_host_arrays("view")[2])
+    S = np.random.default_rng(V).standard_normal((m, n))
+    H.compress(W, H.HiNMConfig(V, 2, 4, 0.5), synth.random_sigma_o(m, V + 1), saliency=S)
+# gyro search kernels on a small instance (OCP + k-means + ICP)
+Wg = synth.randn_bf16((128, 64), 3).astype(np.float64)
+P.gyro_permute(Wg, H.HiNMConfig(32, 2, 4, 0.5, ocp_max_iters=2, icp_max_iters=2, seed=1))
+torch.cuda.synchronize()
 print("sanitize smoke ok")
