@@ -7,14 +7,13 @@
 //   k_tile_sort (cub for n > 16384)   a4  per-tile stable descending sort of the scores (ties ->
 //                      lower column), only over the key bits that differ inside the tile
 //   k_gains        a4  gains[t,q] = numpy-pairwise sum of M sorted scores (+ key OR / AND)
-//   k_budget_coop / k_budget_radix   a5  global greedy == G smallest keys (-gain, q, t)
+//   k_bsel_hist / _collect / _final, k_budget_radix   a5  global greedy == G smallest keys (-gain, q, t)
 //   k_survivors    a6/a7 ascending survivors per tile, vector mask
 //   k_validate_sigma / k_dead_check   a7/a9 invariant checks (pruning.py:196-204, 226-254)
 //   k_select_pack  a8/a10 fused 2:4 select + reference view + tcgen05 operand image + gidx
 //   k_nm_select(_rows), k_pack_*   a8/a10 general N:M / V path and HiNMEncoding -> operand image
 #include <climits>
 #include <cstdlib>
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -543,94 +542,178 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
 }
 
 
-// a5, multi-CTA: radix select of the G-th smallest budget key over the whole grid (cooperative
-// launch).  11-bit digits over only the key bits that differ between some keys (OR / AND words
-// from the gains pass): ~3 passes of one CTA-wide shared histogram each and one grid barrier per
-// pass; then one warp per tile finds its bounds around the threshold key and block 0 applies the
-// (q, t) tie order (budget_tail).
-constexpr int BUDGET_BITS = 11, BUDGET_BINS = 1 << BUDGET_BITS, BUDGET_MAX_PASSES = 6;
+// a5, three plain launches (no grid barrier): (1) a 4096-bin histogram of the top 12 differing
+// bits of every budget key, (2) every CTA finds the bin holding rank G (redundantly, from the
+// 16 KB histogram) and appends the keys of that bin to a candidate list, (3) one CTA selects the
+// exact key among the candidates (block radix sort when they fit, else radix select over the
+// list), finds every tile's bounds around it and applies the (q, t) tie order (budget_tail).
+constexpr int BSEL_BITS = 12, BSEL_BINS = 1 << BSEL_BITS, BSEL_CAP = 4096;
+
+struct BselShape {
+  int shift;        // the bin digit = key bits [shift, shift + BSEL_BITS)
+  uint64_t above;   // mask of the bits above the digit (all keys agree on them)
+};
+__device__ __forceinline__ BselShape bsel_shape(const unsigned long long* keybits) {
+  const uint64_t kor = __ldcg(keybits), kand = __ldcg(keybits + 1), diff = kor ^ kand;
+  const int top = diff ? 63 - __clzll((long long)diff) : BSEL_BITS - 1;
+  BselShape b;
+  b.shift = top - BSEL_BITS + 1 > 0 ? top - BSEL_BITS + 1 : 0;
+  const int hi = b.shift + BSEL_BITS;
+  b.above = hi >= 64 ? 0ull : ~0ull << hi;
+  return b;
+}
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_budget_coop(const double* __restrict__ gains, int T, int G,
-                                                    int64_t total_groups, int M,
-                                                    const unsigned long long* __restrict__ keybits,
-                                                    uint32_t* __restrict__ ghist,
-                                                    int32_t* __restrict__ lo_scr,
-                                                    int32_t* __restrict__ hi_scr,
-                                                    int32_t* __restrict__ tile_ptr) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  constexpr int NW = NT / 32;
-  constexpr int PER = BUDGET_BINS / NT;  // bins per thread in the bucket search
+__global__ void __launch_bounds__(NT) k_bsel_hist(const double* __restrict__ gains, int64_t total,
+                                                  const unsigned long long* __restrict__ keybits,
+                                                  uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t hist[BSEL_BINS];
+  const int lane = threadIdx.x & 31;
+  const BselShape sh = bsel_shape(keybits);
+  for (int i = threadIdx.x; i < BSEL_BINS; i += NT) hist[i] = 0;
+  __syncthreads();
+  for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < total;
+    const uint32_t bin = ok ? (uint32_t)(gain_key(gains[i]) >> sh.shift) & (BSEL_BINS - 1) : 0u;
+    const uint32_t act = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const uint32_t peers = __match_any_sync(act, bin);
+      if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int bn = threadIdx.x; bn < BSEL_BINS; bn += NT)
+    if (hist[bn]) atomicAdd(ghist + bn, hist[bn]);
+}
+
+// the bin holding rank k (1-based) and the rank inside it, from the global histogram (every thread)
+template <int NT>
+__device__ void bsel_find(const uint32_t* __restrict__ ghist, int64_t k, int* s_bin, int64_t* s_k) {
+  constexpr int PER = BSEL_BINS / NT;
   typedef cub::BlockScan<uint32_t, NT> BS;
-  __shared__ uint32_t hist[BUDGET_BINS];
   __shared__ typename BS::TempStorage scan_tmp;
-  __shared__ uint64_t s_prefix;
+  uint32_t c[PER], sum = 0;
+#pragma unroll
+  for (int b2 = 0; b2 < PER; ++b2) {
+    c[b2] = __ldcg(ghist + threadIdx.x * PER + b2);
+    sum += c[b2];
+  }
+  uint32_t excl;
+  BS(scan_tmp).ExclusiveSum(sum, excl);
+  if ((int64_t)excl < k && k <= (int64_t)excl + sum) {
+    int64_t before = excl;
+    int b2 = 0;
+    while (before + c[b2] < k) { before += c[b2]; ++b2; }
+    *s_bin = threadIdx.x * PER + b2;
+    *s_k = k - before;
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ gains, int64_t total,
+                                                     int64_t rank, const unsigned long long* __restrict__ keybits,
+                                                     const uint32_t* __restrict__ ghist,
+                                                     unsigned long long* __restrict__ cand,
+                                                     unsigned int* __restrict__ ncand) {
+  __shared__ int s_bin;
+  __shared__ int64_t s_k;
+  const int lane = threadIdx.x & 31;
+  const BselShape sh = bsel_shape(keybits);
+  bsel_find<NT>(ghist, rank, &s_bin, &s_k);
+  const uint32_t want = (uint32_t)s_bin;
+  for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint64_t d = i < total ? gain_key(gains[i]) : 0;
+    const bool in = i < total && ((uint32_t)(d >> sh.shift) & (BSEL_BINS - 1)) == want;
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (!m) continue;
+    unsigned int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(ncand, (unsigned int)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    const unsigned int slot = base + __popc(m & ((1u << lane) - 1u));
+    if (in && slot < BSEL_CAP) cand[slot] = d;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bsel_final(const double* __restrict__ gains, int T, int G,
+                                                   int64_t total_groups, int M,
+                                                   const unsigned long long* __restrict__ keybits,
+                                                   const uint32_t* __restrict__ ghist,
+                                                   const unsigned long long* __restrict__ cand,
+                                                   const unsigned int* __restrict__ ncand,
+                                                   int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
+                                                   int32_t* __restrict__ tile_ptr) {
+  constexpr int ITEMS = BSEL_CAP / NT;
+  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS> BRS;
+  __shared__ typename BRS::TempStorage sort_tmp;
+  __shared__ uint64_t s_x;
+  __shared__ int s_bin;
   __shared__ int64_t s_k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t total = (int64_t)T * G;
-  // bits on which all keys agree need no pass: they are taken from the AND of the keys
-  const uint64_t kor = __ldcg(keybits), kand = __ldcg(keybits + 1), diff = kor ^ kand;
-  const int top = diff ? 63 - __clzll((long long)diff) : -1;      // highest differing bit
-  const int low = diff ? __ffsll((long long)diff) - 1 : 0;         // lowest differing bit
-  const uint64_t above = top >= 63 ? 0ull : ~0ull << (top + 1);
-  uint64_t prefix = kand & above, pmask = above;
-  int64_t k = total_groups;
-  int pass = 0;
-  for (int hi = top; hi >= low; hi -= BUDGET_BITS, ++pass) {
-    const int shift = hi - BUDGET_BITS + 1 > low ? hi - BUDGET_BITS + 1 : low;  // digit = bits [shift, hi]
-    const int nbits = hi - shift + 1;
-    const uint32_t dmask = (1u << nbits) - 1u;
-    for (int i = threadIdx.x; i < BUDGET_BINS; i += NT) hist[i] = 0;
-    __syncthreads();
-    for (int64_t i0 = (int64_t)blockIdx.x * NT; i0 < total; i0 += (int64_t)gridDim.x * NT) {
-      const int64_t i = i0 + threadIdx.x;
-      const uint64_t d = i < total ? gain_key(gains[i]) : 0;
-      const bool cand = i < total && (d & pmask) == prefix;
-      const uint32_t bin = (uint32_t)(d >> shift) & dmask;
-      const uint32_t act = __ballot_sync(0xffffffffu, cand);
-      if (cand) {
-        const uint32_t peers = __match_any_sync(act, bin);
-        if ((__ffs(peers) - 1) == lane) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
-      }
-    }
-    __syncthreads();
-    uint32_t* gh = ghist + pass * BUDGET_BINS;
-    for (int bn = threadIdx.x; bn < BUDGET_BINS; bn += NT)
-      if (hist[bn]) atomicAdd(gh + bn, hist[bn]);
-    grid.sync();
-    // every CTA finds the bin holding rank k (bins PER per thread, one block scan)
-    uint32_t c[PER], sum = 0;
+  bsel_find<NT>(ghist, total_groups, &s_bin, &s_k);
+  const int64_t kk = s_k;
+  const unsigned int nc = __ldcg(ncand);
+  if (nc <= BSEL_CAP) {
+    uint64_t keys[ITEMS];
 #pragma unroll
-    for (int b2 = 0; b2 < PER; ++b2) {
-      c[b2] = __ldcg(gh + threadIdx.x * PER + b2);
-      sum += c[b2];
+    for (int i = 0; i < ITEMS; ++i) {
+      const unsigned int j = threadIdx.x * ITEMS + i;
+      keys[i] = j < nc ? __ldcg(cand + j) : ~0ull;  // padding sorts last
     }
-    uint32_t excl;
-    BS(scan_tmp).ExclusiveSum(sum, excl);
-    if ((int64_t)excl < k && k <= (int64_t)excl + sum) {
-      int64_t before = excl;
-      int b2 = 0;
-      while (before + c[b2] < k) { before += c[b2]; ++b2; }
-      s_prefix = prefix | ((uint64_t)(threadIdx.x * PER + b2) << shift);
-      s_k = k - before;
+    BRS(sort_tmp).Sort(keys);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if ((int64_t)(threadIdx.x * ITEMS + i) == kk - 1) s_x = keys[i];
+    __syncthreads();
+  } else {
+    // more candidates than fit (a bin holding > BSEL_CAP keys: tie-heavy gains): the bin's keys
+    // agree on their top bits; exact radix select over all keys with that prefix, one CTA
+    const BselShape sh = bsel_shape(keybits);
+    const int64_t total = (int64_t)T * G;
+    uint64_t pmask = sh.above | ((uint64_t)(BSEL_BINS - 1) << sh.shift);
+    uint64_t prefix = (__ldcg(keybits + 1) & sh.above) | ((uint64_t)s_bin << sh.shift);
+    int64_t k = kk;
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ int64_t s_kk;
+    for (int shift = sh.shift - 8; shift > -8; shift -= 8) {
+      const int sft = shift > 0 ? shift : 0;
+      const uint64_t dmask = shift >= 0 ? 0xFFull : (0xFFull >> -shift);
+      for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < total; i += NT) {
+        const uint64_t d = gain_key(gains[i]);
+        if ((d & pmask) == prefix) atomicAdd(&hist[(d >> sft) & dmask], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t before = 0;
+        int b2 = 0;
+        while (before + hist[b2] < k) { before += hist[b2]; ++b2; }
+        s_prefix = prefix | ((uint64_t)b2 << sft);
+        s_kk = k - before;
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      k = s_kk;
+      pmask |= dmask << sft;
+      __syncthreads();
+      if (sft == 0) break;
     }
+    if (threadIdx.x == 0) s_x = prefix;
     __syncthreads();
-    prefix = s_prefix;
-    k = s_k;
-    pmask |= (uint64_t)dmask << shift;
-    __syncthreads();
-    if (shift == low) break;
   }
-  prefix |= kand & ~pmask;  // constant low bits
-  for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {  // one warp per tile
+  const uint64_t x = s_x;
+  for (int t = warp; t < T; t += NT / 32) {  // one warp per tile
     const double* row = gains + (int64_t)t * G;
-    const int a = row_bound_warp(row, G, prefix, false), b = row_bound_warp(row, G, prefix, true);
+    const int a = row_bound_warp(row, G, x, false), b = row_bound_warp(row, G, x, true);
     if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
   }
-  grid.sync();
-  if (blockIdx.x != 0) return;
-  budget_tail<NT>(gains, T, G, total_groups, M, prefix, false, lo_scr, hi_scr, tile_ptr);
+  __syncthreads();
+  budget_tail<NT>(gains, T, G, total_groups, M, x, false, lo_scr, hi_scr, tile_ptr);
 }
 
 // a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
@@ -1218,7 +1301,8 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->hi = take(4 * T);
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
   L->err = take(16);
-  L->ghist = take(BUDGET_MAX_PASSES * BUDGET_BINS * 4 + 16);  // radix histograms + key OR / AND words
+  // budget select: bin histogram + candidate count, candidate keys, key OR / AND words
+  L->ghist = take(BSEL_BINS * 4 + 16 + BSEL_CAP * 8 + 16);
   size_t cb = 0;
   int st = cub_sort_bytes((int)T, n, &cb);
   if (st) return st;
@@ -1353,8 +1437,9 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     HINM_LAUNCH_CHECK();
   }
   uint32_t* ghist = (uint32_t*)(ws + L.ghist);
-  unsigned long long* keybits = (unsigned long long*)(ghist + BUDGET_MAX_PASSES * BUDGET_BINS);
-  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, BUDGET_MAX_PASSES * BUDGET_BINS * 4 + 8, stream));
+  unsigned long long* keybits = (unsigned long long*)(ghist + BSEL_BINS + 4 + 2 * BSEL_CAP);
+  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, BSEL_BINS * 4 + 16, stream));
+  HINM_CUDA_TRY(cudaMemsetAsync(keybits, 0, 8, stream));
   HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
   const bool fused = n <= 16384 && G > 0;
   double* cmin = sorted;  // fused path: per-chunk last score (T x G) in the sorted region
@@ -1378,25 +1463,29 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   {
     int32_t* lo_s = (int32_t*)(ws + L.lo);
     int32_t* hi_s = (int32_t*)(ws + L.hi);
-    static int per_sm = -1, sms = 0;  // device properties, queried once per process
-    if (per_sm < 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
+    static int sms_of[64] = {};  // per-device SM count, queried once
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+      if (!sms_of[dev]) cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev);
+      sms = sms_of[dev];
+    } else {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_budget_coop<1024>, 1024, 0);
     }
     const int64_t total = (int64_t)T * G;
-    // one 1024-key slice per CTA and pass (every SM busy on the LLaMA shapes), at most one wave
-    int nblk = (int)std::min<int64_t>((int64_t)per_sm * sms, std::max<int64_t>(1, ceil_div(total, 1024)));
-    if (per_sm < 1 || nblk < 2) {
+    if (total <= 16384 || sms < 1) {
       k_budget_radix<1024><<<1, 1024, 0, stream>>>(gains, T, G, groups, M, lo_s, hi_s, tile_ptr);
       HINM_LAUNCH_CHECK();
     } else {
-      int Ti = T, Gi = G, Mi = M;
-      int64_t gr = groups;
-      void* args[] = {(void*)&gains, &Ti, &Gi, &gr, &Mi, &keybits, &ghist, &lo_s, &hi_s, &tile_ptr};
-      HINM_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_budget_coop<1024>, dim3(nblk), dim3(1024),
-                                                args, 0, stream));
+      // ghist[0..BSEL_BINS) histogram, then the candidate count and list (zeroed with the histogram)
+      unsigned int* ncand = (unsigned int*)(ghist + BSEL_BINS);
+      unsigned long long* cand = (unsigned long long*)(ghist + BSEL_BINS + 4);
+      const unsigned nblk = (unsigned)std::min<int64_t>(2 * sms, ceil_div(total, 1024));
+      k_bsel_hist<1024><<<nblk, 1024, 0, stream>>>(gains, total, keybits, ghist);
+      k_bsel_collect<1024><<<nblk, 1024, 0, stream>>>(gains, total, groups, keybits, ghist, cand, ncand);
+      k_bsel_final<512><<<1, 512, 0, stream>>>(gains, T, G, groups, M, keybits, ghist, cand, ncand, lo_s, hi_s,
+                                                tile_ptr);
+      HINM_LAUNCH_CHECK();
     }
   }
   if (fused) {

@@ -27,6 +27,10 @@ KEYS = [
     ("launch__block_size", "block"),
     ("launch__registers_per_thread", "registers/thread"),
     ("smsp__sass_inst_executed_op_ldgsts.sum", "LDGSTS instructions"),
+    ("lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed", "L2 sectors from SMs % (avg slice)"),
+    ("lts__t_sectors_srcunit_tex.max.pct_of_peak_sustained_elapsed", "L2 sectors from SMs % (max slice)"),
+    ("lts__lts2xbar_cycles_active.avg.pct_of_peak_sustained_elapsed", "L2->xbar return % (avg slice)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe cycles active %"),
 ]
 
 
