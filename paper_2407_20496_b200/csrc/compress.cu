@@ -3,12 +3,13 @@
 // reduction reproduces numpy's summation order (see common.cuh / oracle/hinm_oracle.py).
 //
 // Kernels:
-//   k_scores4 / k_scores   a3  col_score[t,j] = sum_r S[sigma_o[tV+r], j]  (fp64, sigma_o order)
+//   k_scores8 / k_scores4 / k_scores   a3  col_score[t,j] = sum_r S[sigma_o[tV+r], j]  (fp64, sigma_o order)
 //   k_tile_sort (cub for n > 16384)   a4  per-tile stable descending sort of the scores (ties ->
 //                      lower column), only over the key bits that differ inside the tile
 //   k_gains        a4  gains[t,q] = numpy-pairwise sum of M sorted scores (+ key OR / AND)
 //   k_bsel_hist / _collect / _final, k_budget_radix   a5  global greedy == G smallest keys (-gain, q, t)
-//   k_survivors    a6/a7 ascending survivors per tile, vector mask
+//   k_tile_rank    a4  per-tile bitonic sort (score desc, column asc) + gains + sorted order
+//   k_survivors(_ord)   a6/a7 ascending survivors per tile, vector mask
 //   k_validate_sigma / k_dead_check   a7/a9 invariant checks (pruning.py:196-204, 226-254)
 //   k_select_pack  a8/a10 fused 2:4 select + reference view + tcgen05 operand image + gidx
 //   k_nm_select(_rows), k_pack_*   a8/a10 general N:M / V path and HiNMEncoding -> operand image
@@ -93,6 +94,46 @@ __global__ void __launch_bounds__(NT) k_scores4(const uint16_t* __restrict__ W, 
   double* out = scores + (int64_t)t * n + j0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) out[k] = acc[k] + 0.0;
+}
+
+// a3 (bf16 fast path, n % 8 == 0): 8 consecutive columns per thread (one 16-byte load per row, a
+// warp reads 512 contiguous bytes of a row), 8 rows of loads in flight (128 B per thread), still
+// summed sequentially in sigma_o row order per column.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, int64_t ldw,
+                                                const int32_t* __restrict__ sigma_o, int n, int V,
+                                                double* __restrict__ scores) {
+  extern __shared__ int32_t s_rows8[];
+  const int t = blockIdx.y;
+  for (int r = threadIdx.x; r < V; r += NT) s_rows8[r] = sigma_o[(int64_t)t * V + r];
+  __syncthreads();
+  const int j0 = (blockIdx.x * NT + threadIdx.x) * 8;
+  if (j0 >= n) return;
+  const uint16_t* Wc = W + j0;
+  double acc[8];
+  auto add = [&](uint4 v, bool first) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double lo = bf16_abs_f64((uint16_t)(w[k] & 0xFFFFu));
+      const double hi = bf16_abs_f64((uint16_t)(w[k] >> 16));
+      acc[2 * k] = first ? lo : acc[2 * k] + lo;
+      acc[2 * k + 1] = first ? hi : acc[2 * k + 1] + hi;
+    }
+  };
+  int r = 0;
+  for (; r + 8 <= V; r += 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = __ldcs(reinterpret_cast<const uint4*>(Wc + (int64_t)s_rows8[r + u] * ldw));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add(v[u], r + u == 0);
+  }
+  for (; r < V; ++r) add(__ldcs(reinterpret_cast<const uint4*>(Wc + (int64_t)s_rows8[r] * ldw)), r == 0);
+  double2* out = reinterpret_cast<double2*>(scores + (int64_t)t * n + j0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = make_double2(acc[2 * k] + 0.0, acc[2 * k + 1] + 0.0);
 }
 
 __global__ void k_iota_cols(int32_t* __restrict__ v, int n, int64_t total) {
@@ -260,28 +301,6 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_tile_sort(const doubl
   }
 }
 
-// a4 (fast path, n <= 16384, fused): one CTA per tile sorts the tile's scores descending (keys
-// only: the order-preserving images of the scores, over the bits that differ inside the tile) and
-// writes, per M-chunk of the sorted scores, its gain (numpy summation order) and its last (smallest)
-// score -- everything the budget and the survivor pass need.  No column payload and no sorted copy
-// are written: survivors are recovered from the per-tile threshold score (k_survivors_thr).
-// Radix digit width of the tile sorts: cub's rank counters take 2^(bits-1) x NT x 4 bytes of shared
-// memory, so 1024-thread CTAs use 5-bit digits and smaller CTAs 6-bit digits.
-template <int NT>
-constexpr int tile_radix_bits() { return NT >= 1024 ? 5 : 6; }
-
-template <int NT, int ITEMS>
-struct TileSort {
-  typedef cub::BlockRadixSort<uint32_t, NT, ITEMS, cub::NullType, tile_radix_bits<NT>()> S32;
-  typedef cub::BlockRadixSort<uint32_t, NT, ITEMS, uint32_t, tile_radix_bits<NT>()> P32;
-  static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-  static constexpr size_t bytes =
-      cmax(cmax(sizeof(typename S32::TempStorage), sizeof(typename P32::TempStorage)), (size_t)NT * ITEMS * 8);
-};
-
-template <int NT, int ITEMS>
-__host__ __device__ constexpr size_t tile_gains_smem() { return TileSort<NT, ITEMS>::bytes; }
-
 // numpy's sum of M consecutive values (pairwise_sum: a plain loop below 8 terms)
 template <class Get>
 __device__ __forceinline__ double chunk_sum(const Get& get, int M) {
@@ -293,93 +312,246 @@ __device__ __forceinline__ double chunk_sum(const Get& get, int M) {
   return np_pairwise_sum(get, 0, M);
 }
 
-// a4 (fast path, n <= 16384, fused): one CTA per tile sorts the tile's scores descending (keys
-// only: the order-preserving images of the scores, over the bits that differ inside the tile --
-// as 32-bit keys when those bits span <= 32, the common case: column sums of bf16 magnitudes share
-// their sign / top exponent bits and end in zero mantissa bits) and writes, per M-chunk of the
-// sorted scores, its gain (numpy summation order) and its last (smallest) score -- everything the
-// budget and the survivor pass need.  No column payload and no sorted copy are written: survivors
-// are recovered from the per-tile threshold score (k_survivors_thr).
-template <int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_tile_gains(const double* __restrict__ scores, int n, int M, int G,
-                                                  double* __restrict__ gains, double* __restrict__ cmin,
-                                                  unsigned long long* __restrict__ keybits) {
-  typedef TileSort<NT, ITEMS> TS;
-  typedef cub::BlockReduce<uint64_t, NT> BR;
-  extern __shared__ __align__(16) uint8_t tg_smem[];
-  double* vals = reinterpret_cast<double*>(tg_smem);
-  __shared__ typename BR::TempStorage red_tmp;
-  __shared__ uint64_t s_or, s_and;
+// Ascending bitonic sort of P (a power of two) 64-bit keys in shared memory by all NT threads
+// (WIDE: ties on the key ordered by a 16-bit payload, compared as a second word).  Pair i of a
+// stage compares elements a = 2i - (i mod j) and a + j; with j <= 32 the pairs a warp owns lie in
+// one 64-element block, so those stages need only a warp barrier -- the block barrier is taken
+// where a stage reaches across warps (j > 32) or the next one will (the first stage of the next
+// merge size).
+template <int NT, bool WIDE>
+__device__ __forceinline__ void bitonic_sort_smem(uint64_t* __restrict__ key, uint16_t* __restrict__ pay, int P) {
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += NT) {
+        const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;
+        const bool up = (a & size) == 0 || size == P;
+        const uint64_t ka = key[a], kb = key[b];
+        bool gt = ka > kb;
+        if (WIDE) gt = gt || (ka == kb && pay[a] > pay[b]);
+        if (gt == up) {
+          key[a] = kb;
+          key[b] = ka;
+          if (WIDE) {
+            const uint16_t t = pay[a];
+            pay[a] = pay[b];
+            pay[b] = t;
+          }
+        }
+      }
+      if (j > 32 || (j == 1 && size >= 64 && size < P)) __syncthreads(); else __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__host__ __device__ constexpr int rank_min_blocks() { return NT >= 1024 ? 1 : 2048 / NT / 2; }
+
+constexpr int RANK_PER = 8;        // bucket pass: RANK_PER * NT buckets (4096 / 8192)
+constexpr int RANK_MAXB = 256;     // larger buckets (tie-heavy scores) -> bitonic network instead
+
+__host__ __device__ inline size_t tile_rank_smem(int n, int P) {
+  const int nt = n <= 4096 ? 512 : 1024;
+  const size_t bucket = (size_t)n * 16 + (size_t)RANK_PER * nt * 4;
+  const size_t net = (size_t)P * 10;
+  return bucket > net ? bucket : net;
+}
+
+// a4 (n <= 12032): one CTA per tile orders the tile's columns by (score descending, column
+// ascending) -- np.lexsort((cols, -score)), pruning.py:91 -- and writes per M-chunk of the sorted
+// scores its gain (numpy's summation order, pruning.py:93-94), the sorted column order (uint16: the
+// survivors of a tile are its first k_t entries) and the OR / AND of the budget keys.
+// Sort key: the column packed into the low 14 bits under the complement of the score's varying
+// field (the bits that differ inside the tile: ~20-32 for column sums of bf16 magnitudes), so one
+// 64-bit compare orders (score desc, column asc).  The sort is O(n): a bucket pass (buckets =
+// 8 * NT equal ranges of the key between the tile's min and max, shared-memory histogram, scan,
+// scatter) and then every key's rank inside its bucket by counting the bucket's smaller keys (a
+// few each).  A tile whose scores differ in more than 50 bits (external fp64 saliency) or whose
+// buckets exceed 256 keys (ties) sorts with a bitonic network instead.
+template <int NT>
+__global__ void __launch_bounds__(NT, rank_min_blocks<NT>()) k_tile_rank(
+    const double* __restrict__ scores, int n, int P, int M, int G, double* __restrict__ gains,
+    uint16_t* __restrict__ order16, unsigned long long* __restrict__ keybits) {
+  constexpr int NB = RANK_PER * NT;
+  extern __shared__ __align__(16) uint8_t rk_smem[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(rk_smem);                      // [n] keys, then sorted
+  uint64_t* tmp = key + n;                                                    // [n] bucketed keys
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(rk_smem + (size_t)n * 16);      // [NB]
+  typedef cub::BlockScan<uint32_t, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ unsigned long long s_or, s_and, s_min, s_max;
+  __shared__ int s_maxb;
   const int t = blockIdx.x;
   const double* row = scores + (int64_t)t * n;
+  if (threadIdx.x == 0) { s_or = 0ull; s_and = ~0ull; s_min = ~0ull; s_max = 0ull; s_maxb = 0; }
+  for (int i = threadIdx.x; i < NB; i += NT) cnt[i] = 0u;
+  __syncthreads();
   uint64_t lor = 0, land = ~0ull;
   for (int j = threadIdx.x; j < n; j += NT) {
-    const uint64_t k = ord_key(row[j]);
+    const uint64_t k = ord_key(__ldg(row + j));
+    key[j] = k;
     lor |= k;
     land &= k;
   }
-  lor = BR(red_tmp).Reduce(lor, OrOp());
-  if (threadIdx.x == 0) s_or = lor;
-  __syncthreads();
-  land = BR(red_tmp).Reduce(land, AndOp());
-  if (threadIdx.x == 0) s_and = land;
-  __syncthreads();
-  const uint64_t diff = s_or ^ s_and, base = s_and;
-  const int begin = diff ? __ffsll((long long)diff) - 1 : 0;
-  const int width = diff ? 64 - __clzll((long long)diff) - begin : 0;
-  if (width <= 32) {
-    // key = the varying field; padding 0 sorts after every real key (stable: ties keep order)
-    uint32_t keys[ITEMS];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int j = threadIdx.x * ITEMS + i;
-      keys[i] = j < n ? (uint32_t)((ord_key(row[j]) ^ base) >> begin) : 0u;
-    }
-    if (width) {
-      typename TS::S32::TempStorage& tmp = *reinterpret_cast<typename TS::S32::TempStorage*>(tg_smem);
-      TS::S32(tmp).SortDescending(keys, 0, width);
-      __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) vals[threadIdx.x * ITEMS + i] = ord_value(base | ((uint64_t)keys[i] << begin));
-  } else {
-    // wider fields: two stable 32-bit passes, least significant first (low 32 bits of the field,
-    // then the rest), each carrying the other half as payload
-    uint32_t lo[ITEMS], hi[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int j = threadIdx.x * ITEMS + i;
-      const uint64_t f = j < n ? (ord_key(row[j]) ^ base) >> begin : 0ull;
-      lo[i] = (uint32_t)f;
-      hi[i] = (uint32_t)(f >> 32);
-    }
-    typename TS::P32::TempStorage& tmp = *reinterpret_cast<typename TS::P32::TempStorage*>(tg_smem);
-    TS::P32(tmp).SortDescending(lo, hi, 0, 32);
-    __syncthreads();
-    TS::P32(tmp).SortDescending(hi, lo, 0, width - 32);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      vals[threadIdx.x * ITEMS + i] = ord_value(base | ((((uint64_t)hi[i] << 32) | lo[i]) << begin));
+  for (int o = 16; o; o >>= 1) {
+    lor |= __shfl_xor_sync(0xffffffffu, lor, o);
+    land &= __shfl_xor_sync(0xffffffffu, land, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&s_or, (unsigned long long)lor);
+    atomicAnd(&s_and, (unsigned long long)land);
   }
   __syncthreads();
+  const uint64_t base = s_and, diff = s_or ^ s_and;
+  const int begin = diff ? __ffsll((long long)diff) - 1 : 0;
+  const int width = diff ? 64 - __clzll((long long)diff) - begin : 0;
+  const bool wide = width > 50;
+  const uint64_t fmask = width >= 64 ? ~0ull : ((1ull << width) - 1ull);
+  if (!wide) {
+    uint64_t kmin = ~0ull, kmax = 0ull;
+    for (int j = threadIdx.x; j < n; j += NT) {
+      const uint64_t c = ((~((key[j] ^ base) >> begin) & fmask) << 14) | (uint64_t)j;
+      key[j] = c;
+      kmin = min(kmin, c);
+      kmax = max(kmax, c);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      kmin = min(kmin, (uint64_t)__shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, (uint64_t)__shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_min, (unsigned long long)kmin);
+      atomicMax(&s_max, (unsigned long long)kmax);
+    }
+    __syncthreads();
+    // bucket = floor((c - min) * NB / (max - min + 1)) in double: monotone in c, which is all the
+    // bucket pass needs (buckets are then sorted inside)
+    const uint64_t cmin = s_min;
+    const double scale = (double)NB / ((double)(s_max - cmin) + 1.0);
+    auto bucket = [&](uint64_t c) -> int { return min(NB - 1, (int)((double)(c - cmin) * scale)); };
+    for (int j = threadIdx.x; j < n; j += NT) atomicAdd(&cnt[bucket(key[j])], 1u);
+    __syncthreads();
+    uint32_t c[RANK_PER], sum = 0, mx = 0;
+#pragma unroll
+    for (int i = 0; i < RANK_PER; ++i) {
+      c[i] = cnt[threadIdx.x * RANK_PER + i];
+      sum += c[i];
+      mx = max(mx, c[i]);
+    }
+    uint32_t ex;
+    BS(scan_tmp).ExclusiveSum(sum, ex);
+    if (mx > RANK_MAXB) atomicMax(&s_maxb, (int)mx);
+#pragma unroll
+    for (int i = 0; i < RANK_PER; ++i) {
+      cnt[threadIdx.x * RANK_PER + i] = ex;  // bucket start, advanced to its end by the scatter
+      ex += c[i];
+    }
+    __syncthreads();
+    if (s_maxb == 0) {
+      for (int j = threadIdx.x; j < n; j += NT) {
+        const uint64_t k = key[j];
+        tmp[atomicAdd(&cnt[bucket(k)], 1u)] = k;
+      }
+      __syncthreads();
+      // rank inside the bucket [lo, hi) = #smaller keys there (keys are distinct: column bits)
+      for (int p = threadIdx.x; p < n; p += NT) {
+        const uint64_t k = tmp[p];
+        const int bk = bucket(k);
+        const int lo = bk ? (int)cnt[bk - 1] : 0, hi = (int)cnt[bk];
+        int r = lo;
+        for (int i = lo; i < hi; ++i) r += tmp[i] < k ? 1 : 0;
+        key[r] = k;
+      }
+      __syncthreads();
+    }
+  }
+  const bool net = wide || s_maxb != 0;
+  uint64_t* nk = reinterpret_cast<uint64_t*>(rk_smem);  // network path: P keys (+ P payloads)
+  uint16_t* npay = reinterpret_cast<uint16_t*>(rk_smem + (size_t)P * 8);
+  if (net) {
+    // keys are in key[0..n) (packed, or raw ord keys when wide); the network sorts them in place
+    for (int j = threadIdx.x; j < P; j += NT) {
+      if (j < n) {
+        if (wide) {
+          const uint64_t k = key[j];
+          nk[j] = ~k;  // ascending <=> score descending
+          npay[j] = (uint16_t)j;
+        }
+      } else {
+        nk[j] = ~0ull;  // padding sorts last
+        if (wide) npay[j] = 0xFFFFu;
+      }
+    }
+    if (wide) bitonic_sort_smem<NT, true>(nk, npay, P);
+    else bitonic_sort_smem<NT, false>(nk, npay, P);
+  }
+  const uint64_t* sorted = nk;  // both paths leave the sorted keys at the start of shared memory
+  auto score_at = [&](int r) -> double {
+    const uint64_t c = sorted[r];
+    return wide ? ord_value(~c) : ord_value(base | ((~(c >> 14) & fmask) << begin));
+  };
+  uint16_t* ord = order16 + (int64_t)t * n;
+  for (int r = threadIdx.x; r < n; r += NT) ord[r] = wide ? npay[r] : (uint16_t)(sorted[r] & 0x3FFFu);
   uint64_t kor = 0, kand = ~0ull;
   for (int q = threadIdx.x; q < G; q += NT) {
-    const double* c = vals + (int64_t)q * M;
-    auto get = [&](int64_t k) { return c[k]; };
+    auto get = [&](int64_t k) { return score_at(q * M + (int)k); };
     const double g = chunk_sum(get, M) + 0.0;
     gains[(int64_t)t * G + q] = g;
-    cmin[(int64_t)t * G + q] = c[M - 1];
     const uint64_t k = gain_key(g);
     kor |= k;
     kand &= k;
   }
-  kor = BR(red_tmp).Reduce(kor, OrOp());
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+    kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+  }
   __syncthreads();
-  kand = BR(red_tmp).Reduce(kand, AndOp());
-  if (threadIdx.x == 0) {  // one atomic pair per tile (not per warp)
-    atomicOr(keybits, (unsigned long long)kor);
-    atomicAnd(keybits + 1, (unsigned long long)kand);
+  if (threadIdx.x == 0) { s_or = 0ull; s_and = ~0ull; }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&s_or, (unsigned long long)kor);
+    atomicAnd(&s_and, (unsigned long long)kand);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one atomic pair per tile
+    atomicOr(keybits, s_or);
+    atomicAnd(keybits + 1, s_and);
+  }
+}
+
+// a6/a7: survivors of tile t = its first k_t sorted columns, emitted in ascending column order
+// (the default sigma_i, pruning.py:167-169) with the vector mask row: flag the k_t columns, then
+// one block scan over contiguous per-thread column ranges.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict__ order16, int n,
+                                                      const int32_t* __restrict__ tile_ptr,
+                                                      int32_t* __restrict__ surv, uint8_t* __restrict__ vmask) {
+  extern __shared__ __align__(16) uint8_t sv_flags[];
+  typedef cub::BlockScan<int, NT> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
+  const int t = blockIdx.x;
+  const int b0 = tile_ptr[t], k = tile_ptr[t + 1] - b0;
+  const int nw = (n + 15) / 16;
+  for (int i = threadIdx.x; i < nw; i += NT) reinterpret_cast<uint4*>(sv_flags)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const uint16_t* ord = order16 + (int64_t)t * n;
+  for (int i = threadIdx.x; i < k; i += NT) sv_flags[__ldg(ord + i)] = 1;
+  __syncthreads();
+  const int C = (n + NT - 1) / NT, c0 = threadIdx.x * C, c1 = min(n, c0 + C);
+  int cnt = 0;
+  for (int c = c0; c < c1; ++c) cnt += sv_flags[c];
+  int off;
+  BS(scan_tmp).ExclusiveSum(cnt, off);
+  int32_t* out = surv + b0 + off;
+  for (int c = c0; c < c1; ++c)
+    if (sv_flags[c]) *out++ = c;
+  if (vmask) {
+    uint8_t* vm = vmask + (int64_t)t * n;
+    for (int j = threadIdx.x; j < n; j += NT) vm[j] = sv_flags[j];
   }
 }
 
@@ -637,36 +809,31 @@ __global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ 
   }
 }
 
+// The threshold key x = the total_groups-th smallest budget key (one CTA): the rank's bin from the
+// global histogram, then the bitonic-sorted candidates of that bin (or, when a tie-heavy bin holds
+// more keys than the candidate list, an exact 8-bit radix select restricted to the bin's prefix).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_bsel_final(const double* __restrict__ gains, int T, int G,
-                                                   int64_t total_groups, int M,
-                                                   const unsigned long long* __restrict__ keybits,
-                                                   const uint32_t* __restrict__ ghist,
-                                                   const unsigned long long* __restrict__ cand,
-                                                   const unsigned int* __restrict__ ncand,
-                                                   int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
-                                                   int32_t* __restrict__ tile_ptr) {
-  constexpr int ITEMS = BSEL_CAP / NT;
-  typedef cub::BlockRadixSort<uint64_t, NT, ITEMS> BRS;
-  __shared__ typename BRS::TempStorage sort_tmp;
+__global__ void __launch_bounds__(NT) k_bsel_pick(const double* __restrict__ gains, int T, int G,
+                                                  int64_t total_groups,
+                                                  const unsigned long long* __restrict__ keybits,
+                                                  const uint32_t* __restrict__ ghist,
+                                                  const unsigned long long* __restrict__ cand,
+                                                  const unsigned int* __restrict__ ncand,
+                                                  unsigned long long* __restrict__ xsel) {
+  __shared__ uint64_t s_cand[BSEL_CAP];
   __shared__ uint64_t s_x;
   __shared__ int s_bin;
   __shared__ int64_t s_k;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bsel_find<NT>(ghist, total_groups, &s_bin, &s_k);
   const int64_t kk = s_k;
   const unsigned int nc = __ldcg(ncand);
   if (nc <= BSEL_CAP) {
-    uint64_t keys[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const unsigned int j = threadIdx.x * ITEMS + i;
-      keys[i] = j < nc ? __ldcg(cand + j) : ~0ull;  // padding sorts last
-    }
-    BRS(sort_tmp).Sort(keys);
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      if ((int64_t)(threadIdx.x * ITEMS + i) == kk - 1) s_x = keys[i];
+    // the kk-th smallest candidate: bitonic sort of the bin's keys (a few hundred on N(0,1) gains)
+    int P = 2;
+    while (P < (int)nc) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += NT) s_cand[i] = i < (int)nc ? __ldcg(cand + i) : ~0ull;
+    bitonic_sort_smem<NT, false>(s_cand, nullptr, P);
+    if (threadIdx.x == 0) s_x = s_cand[kk - 1];
     __syncthreads();
   } else {
     // more candidates than fit (a bin holding > BSEL_CAP keys: tie-heavy gains): the bin's keys
@@ -706,14 +873,36 @@ __global__ void __launch_bounds__(NT) k_bsel_final(const double* __restrict__ ga
     if (threadIdx.x == 0) s_x = prefix;
     __syncthreads();
   }
-  const uint64_t x = s_x;
-  for (int t = warp; t < T; t += NT / 32) {  // one warp per tile
-    const double* row = gains + (int64_t)t * G;
-    const int a = row_bound_warp(row, G, x, false), b = row_bound_warp(row, G, x, true);
-    if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
-  }
-  __syncthreads();
-  budget_tail<NT>(gains, T, G, total_groups, M, x, false, lo_scr, hi_scr, tile_ptr);
+  if (threadIdx.x == 0) *xsel = s_x;
+}
+
+// Per-tile bounds around x, one warp per tile (all tiles in parallel: the 32-ary searches are
+// latency-bound, a single CTA walking ~10 tiles per warp took ~20 us on the LLaMA shapes).
+__global__ void __launch_bounds__(256) k_bsel_bounds(const double* __restrict__ gains, int T, int G,
+                                                     const unsigned long long* __restrict__ xsel,
+                                                     int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const uint64_t x = __ldcg(xsel);
+  const double* row = gains + (int64_t)t * G;
+  const int a = row_bound_warp(row, G, x, false);
+  // ties of x inside a tile are rare: scan up from the lower bound before the full search
+  int b = a;
+  const int p = a + lane;
+  const bool eq = p < G && gain_key(row[p]) == x;
+  const uint32_t m = __ballot_sync(0xffffffffu, !eq);
+  b = m ? a + __ffs(m) - 1 : row_bound_warp(row, G, x, true);
+  if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
+}
+
+// Per-tile counts with the (q, t) tie order, written as the tile_ptr prefix (one CTA).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bsel_tail(const double* __restrict__ gains, int T, int G,
+                                                  int64_t total_groups, int M,
+                                                  const unsigned long long* __restrict__ xsel,
+                                                  int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
+                                                  int32_t* __restrict__ tile_ptr) {
+  budget_tail<NT>(gains, T, G, total_groups, M, __ldcg(xsel), false, lo_scr, hi_scr, tile_ptr);
 }
 
 // a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
@@ -745,53 +934,6 @@ __global__ void __launch_bounds__(NT) k_survivors(const int32_t* __restrict__ or
     if (f) out[carry + ex] = j;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-}
-
-// a6/a7 from the threshold: survivors of tile t = the k_t best columns by (score desc, column asc)
-// (lexsort, pruning.py:91-93, 163) = every column scoring above s* = the k_t-th largest score (the
-// last score of chunk k_t / M - 1) plus the lowest-indexed columns scoring exactly s*.  Emitted in
-// ascending column order (the default sigma_i, pruning.py:167-169) with the vector mask row.
-template <int NT>
-__global__ void __launch_bounds__(NT) k_survivors_thr(const double* __restrict__ scores, int n, int M, int G,
-                                                      const double* __restrict__ cmin,
-                                                      const int32_t* __restrict__ tile_ptr,
-                                                      int32_t* __restrict__ surv, uint8_t* __restrict__ vmask) {
-  typedef cub::BlockScan<int, NT> BS;
-  __shared__ typename BS::TempStorage scan_tmp;
-  __shared__ int64_t red;
-  __shared__ int carry_tie, carry_out;
-  const int t = blockIdx.x;
-  const int k = tile_ptr[t + 1] - tile_ptr[t];
-  const double* row = scores + (int64_t)t * n;
-  uint8_t* vm = vmask ? vmask + (int64_t)t * n : nullptr;
-  if (k == 0) {
-    if (vm)
-      for (int j = threadIdx.x; j < n; j += NT) vm[j] = 0;
-    return;
-  }
-  const double thr = cmin[(int64_t)t * G + k / M - 1];
-  int64_t above = 0;
-  for (int j = threadIdx.x; j < n; j += NT) above += row[j] > thr ? 1 : 0;
-  const int need = k - (int)block_sum64<NT>(above, &red);  // columns scoring exactly thr to keep
-  if (threadIdx.x == 0) { carry_tie = 0; carry_out = 0; }
-  __syncthreads();
-  int32_t* out = surv + tile_ptr[t];
-  for (int base = 0; base < n; base += NT) {
-    const int j = base + threadIdx.x;
-    const double v = j < n ? row[j] : 0.0;
-    const int tie = (j < n && v == thr) ? 1 : 0;
-    int tex, ttot;
-    BS(scan_tmp).ExclusiveSum(tie, tex, ttot);
-    __syncthreads();
-    const int keep = (j < n && (v > thr || (tie && carry_tie + tex < need))) ? 1 : 0;
-    int kex, ktot;
-    BS(scan_tmp).ExclusiveSum(keep, kex, ktot);
-    if (keep) out[carry_out + kex] = j;
-    if (vm && j < n) vm[j] = (uint8_t)keep;
-    __syncthreads();
-    if (threadIdx.x == 0) { carry_tie += ttot; carry_out += ktot; }
     __syncthreads();
   }
 }
@@ -1260,6 +1402,220 @@ __global__ void __launch_bounds__(NT) k_select_pack(
   }
 }
 
+// a8/a10 fused, streamed: one CTA per (tile, 16 rows).  The weight rows are streamed through a
+// shared-memory ring by 1-D bulk copies (one 2n-byte copy per row, mbarrier completion, NSLOT rows
+// in flight) and consumed four rows at a time; a thread takes one 16-K chunk (4 groups) of two
+// adjacent rows, so the tile's gather indices are read once per row pair and the two rows' a_vals
+// core-matrix rows (adjacent 16-byte halves of a 32-byte sector) leave in one 32-byte store.  The
+// top-2 of 4 is branch-free and does both rows in halfword lanes: six pairwise compares (ties ->
+// lower position, the stable argsort of pruning.py:176), one majority per element, kept positions =
+// first / last set bit of the mask, values by one byte permute.  Same outputs as k_select_pack.
+__device__ __forceinline__ void sp_mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+}
+
+// Two rows at once (halfword lanes: row A low, row B high).  x_c = |v_c(A)| | |v_c(B)| << 16 (15-bit
+// magnitudes); element i is kept iff at most one element beats it (j < i beats on >=, j > i on >):
+// per halfword, "a >= b" is bit 15 of (a | 0x8000) - b (no borrow crosses a halfword), and "not two
+// of three beaters" is one 3-input majority.  Returns the 4-bit kept masks of both rows.
+__device__ __forceinline__ void kept2(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& mA, uint32_t& mB) {
+  constexpr uint32_t H = 0x80008000u;
+  const uint32_t c01 = ((x0 | H) - x1) & H, c02 = ((x0 | H) - x2) & H, c03 = ((x0 | H) - x3) & H;
+  const uint32_t c12 = ((x1 | H) - x2) & H, c13 = ((x1 | H) - x3) & H, c23 = ((x2 | H) - x3) & H;
+  auto maj = [](uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); };
+  const uint32_t k0 = ~maj(~c01, ~c02, ~c03) & H;  // beaters of 0: 1, 2, 3 (strictly greater)
+  const uint32_t k1 = ~maj(c01, ~c12, ~c13) & H;
+  const uint32_t k2 = ~maj(c02, c12, ~c23) & H;
+  const uint32_t k3 = ~maj(c03, c13, c23) & H;
+  const uint32_t comb = (k0 >> 3) | (k1 >> 2) | (k2 >> 1) | k3;  // bits 12..15 row A, 28..31 row B
+  mA = (comb >> 12) & 0xFu;
+  mB = comb >> 28;
+}
+
+// kept mask -> values of the first / last kept positions (w01 = v0 | v1 << 16, w23 = v2 | v3 << 16),
+// reference positions p0 | p1 << 8, metadata nibble p0 | p1 << 2
+__device__ __forceinline__ void from_mask(uint32_t m, uint32_t w01, uint32_t w23, uint32_t& pos, uint32_t& vals,
+                                          uint32_t& nib) {
+  const uint32_t p0 = __ffs(m) - 1, p1 = 31 - __clz(m);
+  vals = __byte_perm(w01, w23, (p0 * 0x22u + 0x10u) | ((p1 * 0x22u + 0x10u) << 8));
+  pos = p0 | (p1 << 8);
+  nib = p0 | (p1 << 2);
+}
+
+constexpr int SP2_ROWS = 16;
+constexpr int SP2_CWARPS = 8;  // consumer warps; warp 8 is the producer
+
+// Producer warp 8: the tile's gather indices (one bulk copy of the k int32 column ids) and the 16
+// weight rows through the ring, each slot refilled as soon as all consumer warps released it
+// (per-slot full / empty mbarriers, no CTA-wide barrier in the loop).  Consumer warps 0-7: rows in
+// quads; warp w takes items w * 32 + lane (+ 256 ...) of the quad, item = (16-K chunk, row pair).
+// DBG (experiments build only, results garbage): 1 = rows streamed, no select / stores; 2 = select and
+// stores on whatever the ring holds, no row copies.
+template <int DBG = 0>
+__global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
+    const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
+    const int32_t* __restrict__ sig_ptr, const int32_t* __restrict__ sig_idx, int n, int V, int nslot,
+    const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
+    uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
+    uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
+  constexpr int NC = 32 * SP2_CWARPS;
+  extern __shared__ __align__(128) uint8_t sp2_smem[];
+  __shared__ __align__(8) uint64_t full[16], empty[16], idx_bar;
+  const int t = blockIdx.y, r0 = blockIdx.x * SP2_ROWS;
+  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
+  const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
+  const int eofs = eofs_g[t], nblk = eofs_g[t + 1] - eofs;
+  if (kp == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = (uint32_t)n * 2;  // host: n % 8 == 0
+  uint8_t* s_rows = sp2_smem;
+  int32_t* s_idx = reinterpret_cast<int32_t*>(sp2_smem + (size_t)nslot * row_bytes);
+  const uint32_t rows_u32 = (uint32_t)__cvta_generic_to_shared(s_rows);
+  const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(full);
+  const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(empty);
+  const uint32_t ibar = (uint32_t)__cvta_generic_to_shared(&idx_bar);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslot; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(SP2_CWARPS));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ibar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nrows = min(SP2_ROWS, V - r0);
+  if (warp == SP2_CWARPS) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      auto bulk = [&](uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(src), "r"(bytes), "r"(bar)
+                     : "memory");
+      };
+      bulk((uint32_t)__cvta_generic_to_shared(s_idx), sig_idx + b, (uint32_t)k * 4, ibar);  // k % 4 == 0
+      int32_t rows[SP2_ROWS];
+#pragma unroll
+      for (int i = 0; i < SP2_ROWS; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
+#pragma unroll
+      for (int rr = 0; rr < SP2_ROWS; ++rr) {
+        if (rr >= nrows) break;
+        const int slot = rr % nslot, use = rr / nslot;
+        if (use > 0) {
+          sp_mbar_wait(empty0 + 8 * slot, (use - 1) & 1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+        }
+        if (DBG == 2)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * slot) : "memory");
+        else
+          bulk(rows_u32 + slot * row_bytes, W + (int64_t)rows[rr] * ldw, row_bytes, full0 + 8 * slot);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  sp_mbar_wait(ibar, 0);
+  if (r0 == 0)  // gather index image: the k real ids, padding repeats the last one
+    for (int i = threadIdx.x; i < kp; i += NC) gidx[kofs + i] = s_idx[i < k ? i : k - 1];
+  const int64_t ref_base = (int64_t)V * (b / 4) * 2;
+  const int nch = kp / 16;        // 16-K chunks with values
+  const int nch_meta = nblk * 8;  // chunks covered by metadata blocks (>= nch)
+  const int nfull = G / 4;        // chunks whose 4 groups are all real
+  uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
+  const int4* s_idx4 = reinterpret_cast<const int4*>(s_idx);
+  for (int rq = 0; rq < nrows; rq += 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sp_mbar_wait(full0 + 8 * ((rq + q) % nslot), ((rq + q) / nslot) & 1);
+    for (int it = warp * 32 + lane; it < (DBG == 1 ? 0 : nch_meta * 2); it += NC) {
+      const int ch = it >> 1, rr = rq + 2 * (it & 1), r = r0 + rr;  // rows r, r + 1
+      const uint16_t* rowA = reinterpret_cast<const uint16_t*>(s_rows + (size_t)(rr % nslot) * row_bytes);
+      const uint16_t* rowB = reinterpret_cast<const uint16_t*>(s_rows + (size_t)((rr + 1) % nslot) * row_bytes);
+      const int g0 = ch * 4;
+      uint32_t pa[4], va[4], pb[4], vb[4], ba = 0, bb = 0;
+      if (ch < nfull) {
+        // all four groups real: every shared-memory load of the chunk issued before any compare
+        int4 i4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) i4[c] = s_idx4[g0 + c];
+        uint32_t av[16], bv[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          av[4 * c] = rowA[i4[c].x]; av[4 * c + 1] = rowA[i4[c].y]; av[4 * c + 2] = rowA[i4[c].z]; av[4 * c + 3] = rowA[i4[c].w];
+          bv[4 * c] = rowB[i4[c].x]; bv[4 * c + 1] = rowB[i4[c].y]; bv[4 * c + 2] = rowB[i4[c].z]; bv[4 * c + 3] = rowB[i4[c].w];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t* a = av + 4 * c;
+          const uint32_t* bq = bv + 4 * c;
+          uint32_t mA, mB, nb;
+          kept2(__byte_perm(a[0], bq[0], 0x5410) & 0x7FFF7FFFu, __byte_perm(a[1], bq[1], 0x5410) & 0x7FFF7FFFu,
+                __byte_perm(a[2], bq[2], 0x5410) & 0x7FFF7FFFu, __byte_perm(a[3], bq[3], 0x5410) & 0x7FFF7FFFu, mA, mB);
+          from_mask(mA, __byte_perm(a[0], a[1], 0x5410), __byte_perm(a[2], a[3], 0x5410), pa[c], va[c], nb);
+          ba |= nb << (4 * c);
+          from_mask(mB, __byte_perm(bq[0], bq[1], 0x5410), __byte_perm(bq[2], bq[3], 0x5410), pb[c], vb[c], nb);
+          bb |= nb << (4 * c);
+        }
+      } else {  // the tile's last chunks: real groups below G, padding above
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int g = g0 + c;
+          if (g < G) {
+            const int4 i4 = s_idx4[g];
+            const uint32_t a0 = rowA[i4.x], a1 = rowA[i4.y], a2 = rowA[i4.z], a3 = rowA[i4.w];
+            const uint32_t b0 = rowB[i4.x], b1 = rowB[i4.y], b2 = rowB[i4.z], b3 = rowB[i4.w];
+            uint32_t mA, mB, nb;
+            kept2(__byte_perm(a0, b0, 0x5410) & 0x7FFF7FFFu, __byte_perm(a1, b1, 0x5410) & 0x7FFF7FFFu,
+                  __byte_perm(a2, b2, 0x5410) & 0x7FFF7FFFu, __byte_perm(a3, b3, 0x5410) & 0x7FFF7FFFu, mA, mB);
+            from_mask(mA, __byte_perm(a0, a1, 0x5410), __byte_perm(a2, a3, 0x5410), pa[c], va[c], nb);
+            ba |= nb << (4 * c);
+            from_mask(mB, __byte_perm(b0, b1, 0x5410), __byte_perm(b2, b3, 0x5410), pb[c], vb[c], nb);
+            bb |= nb << (4 * c);
+          } else {  // padding group: positions {0, 1}, zero values
+            pa[c] = pb[c] = 0x100u;
+            va[c] = vb[c] = 0u;
+            ba |= 0x4u << (4 * c);
+            bb |= 0x4u << (4 * c);
+          }
+        }
+      }
+      if (g0 < G) {  // reference view (real groups only)
+        const int64_t rbA = ref_base + (int64_t)r * G * 2, rbB = rbA + (int64_t)G * 2;
+        if (ch < nfull && (rbA & 7) == 0 && (rbB & 7) == 0) {
+          *reinterpret_cast<uint2*>(nm_pos + rbA + (int64_t)g0 * 2) = make_uint2(pa[0] | (pa[1] << 16), pa[2] | (pa[3] << 16));
+          *reinterpret_cast<uint4*>(kept + rbA + (int64_t)g0 * 2) = make_uint4(va[0], va[1], va[2], va[3]);
+          *reinterpret_cast<uint2*>(nm_pos + rbB + (int64_t)g0 * 2) = make_uint2(pb[0] | (pb[1] << 16), pb[2] | (pb[3] << 16));
+          *reinterpret_cast<uint4*>(kept + rbB + (int64_t)g0 * 2) = make_uint4(vb[0], vb[1], vb[2], vb[3]);
+        } else {
+          for (int c = 0; c < 4 && g0 + c < G; ++c) {
+            reinterpret_cast<uint16_t*>(nm_pos + rbA)[g0 + c] = (uint16_t)pa[c];
+            reinterpret_cast<uint32_t*>(kept + rbA)[g0 + c] = va[c];
+            reinterpret_cast<uint16_t*>(nm_pos + rbB)[g0 + c] = (uint16_t)pb[c];
+            reinterpret_cast<uint32_t*>(kept + rbB)[g0 + c] = vb[c];
+          }
+        }
+      }
+      if (ch < nch) {  // rows r (even) and r + 1: adjacent 16-byte core-matrix rows = one 32-byte sector
+        uint16_t* dst = a_vals + aval_offset(kofs, V, r, 2 * g0);
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(va[0]), "r"(va[1]),
+                     "r"(va[2]), "r"(va[3]), "r"(vb[0]), "r"(vb[1]), "r"(vb[2]), "r"(vb[3])
+                     : "memory");
+      }
+      const int eb = g0 >> 5, w = (g0 >> 3) & 3, k1 = (g0 >> 2) & 1;
+      const int m0 = r & 7, m1 = (r >> 3) & 1, m2 = r >> 4;
+      const int64_t mi = (((int64_t)eb * V + m0 + 8 * k1 + 16 * m2) * 4 + w) * 2 + m1;
+      meta16[mi] = (uint16_t)ba;
+      meta16[mi + 8] = (uint16_t)bb;  // row r + 1: lane m0 + 1
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int q = 0; q < 4; ++q)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * ((rq + q) % nslot)) : "memory");
+  }
+}
+
 }  // namespace hinm
 
 // ---------------------------------------------------------------------------------------------
@@ -1302,7 +1658,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
   L->err = take(16);
   // budget select: bin histogram + candidate count, candidate keys, key OR / AND words
-  L->ghist = take(BSEL_BINS * 4 + 16 + BSEL_CAP * 8 + 16);
+  L->ghist = take(BSEL_BINS * 4 + 16 + BSEL_CAP * 8 + 24);  // + key OR / AND words, threshold key
   size_t cb = 0;
   int st = cub_sort_bytes((int)T, n, &cb);
   if (st) return st;
@@ -1344,26 +1700,24 @@ int launch_tile_sort(const double* scores, int n, int T, double* sorted, int32_t
   return launch_tile_sort_items<16>(scores, n, T, sorted, order, stream);
 }
 
-template <int NT, int ITEMS>
-int launch_tile_gains_items(const double* scores, int n, int T, int M, int G, double* gains, double* cmin,
-                            unsigned long long* keybits, cudaStream_t stream) {
-  constexpr size_t smem = tile_gains_smem<NT, ITEMS>();
-  HINM_CUDA_TRY(smem_optin((const void*)k_tile_gains<NT, ITEMS>, (int)smem));
-  k_tile_gains<NT, ITEMS><<<T, NT, smem, stream>>>(scores, n, M, G, gains, cmin, keybits);
+// Tile sort + gains: 512-thread CTAs (two per SM: the 172 tiles of a LLaMA up projection sort in
+// one wave) up to n = 4096, 1024 threads above.
+int launch_tile_rank(const double* scores, int n, int T, int M, int G, double* gains, uint16_t* order16,
+                     unsigned long long* keybits, cudaStream_t stream) {
+  int P = 2;
+  while (P < n) P <<= 1;
+  const size_t smem = tile_rank_smem(n, P);
+  if (n <= 4096) {
+    // dynamic + static shared memory may pass 48 KB while the dynamic part alone does not: opt in
+    // with slack for the static part
+    HINM_CUDA_TRY(smem_optin((const void*)k_tile_rank<512>, (int)smem + 4096));
+    k_tile_rank<512><<<T, 512, smem, stream>>>(scores, n, P, M, G, gains, order16, keybits);
+  } else {
+    HINM_CUDA_TRY(smem_optin((const void*)k_tile_rank<1024>, (int)smem + 4096));
+    k_tile_rank<1024><<<T, 1024, smem, stream>>>(scores, n, P, M, G, gains, order16, keybits);
+  }
   HINM_LAUNCH_CHECK();
   return HINM_OK;
-}
-
-int launch_tile_gains(const double* scores, int n, int T, int M, int G, double* gains, double* cmin,
-                      unsigned long long* keybits, cudaStream_t stream) {
-  if (n <= 1024) return launch_tile_gains_items<256, 4>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  if (n <= 2048) return launch_tile_gains_items<256, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  if (n <= 4096) return launch_tile_gains_items<512, 8>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  // 512-thread CTAs keep the keys (and the payload of the wide-field path) in registers: 1024
-  // threads would cap every thread at 64 registers and spill
-  if (n <= 8192) return launch_tile_gains_items<512, 16>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  if (n <= 11264) return launch_tile_gains_items<512, 22>(scores, n, T, M, G, gains, cmin, keybits, stream);
-  return launch_tile_gains_items<512, 32>(scores, n, T, M, G, gains, cmin, keybits, stream);
 }
 
 int status_from_rank(int code, int mask_mode) {
@@ -1423,7 +1777,10 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   double* gains = (double*)(ws + L.gains);
   Src src{W, ldw, Wd, ldwd, S, lds};
 
-  if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
+  if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
+    k_scores8<128><<<dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream>>>(
+        W, ldw, sigma_o, n, V, scores);
+  } else if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
     k_scores4<128><<<dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream>>>(
         W, ldw, sigma_o, n, V, scores);
   } else {
@@ -1441,10 +1798,12 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, BSEL_BINS * 4 + 16, stream));
   HINM_CUDA_TRY(cudaMemsetAsync(keybits, 0, 8, stream));
   HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
-  const bool fused = n <= 16384 && G > 0;
-  double* cmin = sorted;  // fused path: per-chunk last score (T x G) in the sorted region
+  int P2 = 2;
+  while (P2 < n) P2 <<= 1;
+  const bool fused = n <= 16384 && G > 0 && tile_rank_smem(n, P2) <= 220 * 1024;
+  uint16_t* order16 = reinterpret_cast<uint16_t*>(sorted);  // fused path: sorted column order (T x n)
   if (fused) {
-    int st2 = launch_tile_gains(scores, n, T, M, G, gains, cmin, keybits, stream);
+    int st2 = launch_tile_rank(scores, n, T, M, G, gains, order16, keybits, stream);
     if (st2) return st2;
   } else if (n <= 16384) {
     // one CTA per tile, stable block radix sort (descending)
@@ -1480,16 +1839,22 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
       // ghist[0..BSEL_BINS) histogram, then the candidate count and list (zeroed with the histogram)
       unsigned int* ncand = (unsigned int*)(ghist + BSEL_BINS);
       unsigned long long* cand = (unsigned long long*)(ghist + BSEL_BINS + 4);
-      const unsigned nblk = (unsigned)std::min<int64_t>(2 * sms, ceil_div(total, 1024));
+      // few CTAs with several keys per thread: every CTA flushes its shared histogram with global
+      // atomics and scans the global one, so 2 x SMs CTAs spent their time on those fixed costs
+      unsigned long long* xsel = keybits + 2;
+      const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms / 4, ceil_div(total, 4096)));
       k_bsel_hist<1024><<<nblk, 1024, 0, stream>>>(gains, total, keybits, ghist);
       k_bsel_collect<1024><<<nblk, 1024, 0, stream>>>(gains, total, groups, keybits, ghist, cand, ncand);
-      k_bsel_final<512><<<1, 512, 0, stream>>>(gains, T, G, groups, M, keybits, ghist, cand, ncand, lo_s, hi_s,
-                                                tile_ptr);
+      k_bsel_pick<512><<<1, 512, 0, stream>>>(gains, T, G, groups, keybits, ghist, cand, ncand, xsel);
+      k_bsel_bounds<<<(unsigned)ceil_div(T, 8), 256, 0, stream>>>(gains, T, G, xsel, lo_s, hi_s);
+      k_bsel_tail<512><<<1, 512, 0, stream>>>(gains, T, G, groups, M, xsel, lo_s, hi_s, tile_ptr);
       HINM_LAUNCH_CHECK();
     }
   }
   if (fused) {
-    k_survivors_thr<1024><<<T, 1024, 0, stream>>>(scores, n, M, G, cmin, tile_ptr, surv, vector_mask);
+    const size_t fsm = (size_t)round_up(n, 16);
+    HINM_CUDA_TRY(smem_optin((const void*)k_survivors_ord<512>, (int)fsm + 4096));
+    k_survivors_ord<512><<<T, 512, fsm, stream>>>(order16, n, tile_ptr, surv, vector_mask);
     HINM_LAUNCH_CHECK();
     return HINM_OK;
   }
@@ -1645,13 +2010,34 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
     k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
     HINM_LAUNCH_CHECK();
-    // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory (measured: 4 rows
-    // staged at once with a shared index load, or the operand image staged and written coalesced,
-    // were both slower on the LLaMA shapes -- 84-101 us vs 56-60 us per layer)
-    HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
-    k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
-        W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
-        p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+    // streamed variant (k_select_pack2): rows bulk-copied through a ring, 16 rows per CTA; needs
+    // 16-byte rows (n % 8 == 0) and a ring of >= 2 rows in ~100 KB (two CTAs per SM)
+    const size_t rowb = (size_t)p->n * 2;
+    // ring: 8 rows when they fit in ~100 KB (several CTAs per SM), else 4 or 8 rows in one CTA per SM
+    int nslot = 8 * rowb <= 100 * 1024 ? 8 : 8 * rowb <= 190 * 1024 ? 8 : 4 * rowb <= 190 * 1024 ? 4 : 0;
+#ifdef HINM_EXPERIMENTS
+    if (const char* e = getenv("HINM_SP2_SLOTS")) nslot = atoi(e);
+#endif
+    const size_t s2 = (size_t)nslot * rowb + (size_t)round_up(kp_cap * 4, 16);
+    const bool streamed = (p->n % 8) == 0 && p->n <= 65536 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0 &&
+                          nslot >= 4 && p->V % SP2_ROWS == 0 && s2 <= 200 * 1024 &&
+                          ((uintptr_t)p->a_vals & 31) == 0 && ((uintptr_t)si & 15) == 0;
+    if (streamed) {
+      auto kern = k_select_pack2<0>;
+#ifdef HINM_EXPERIMENTS
+      if (const char* e = getenv("HINM_SP2")) kern = e[0] == '1' ? k_select_pack2<1> : e[0] == '2' ? k_select_pack2<2> : kern;
+#endif
+      HINM_CUDA_TRY(smem_optin((const void*)kern, (int)s2 + 4096));
+      kern<<<dim3(p->V / SP2_ROWS, p->T), 32 * (SP2_CWARPS + 1), s2, stream>>>(
+          W, ldw, sigma_o, sp, si, p->n, p->V, nslot, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
+          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+    } else {
+      // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory
+      HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
+      k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
+          W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
+          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+    }
     HINM_LAUNCH_CHECK();
     int rc = HINM_OK;
     if (rc) return rc;

@@ -20,6 +20,13 @@ for V, m, n, B in ((64, 256, 512, 264), (32, 128, 256, 64), (128, 256, 384, 136)
     assert np.array_equal(pack.to_host_arrays("image")[2], pack.to_host_arrays("view")[2])
     S = np.random.default_rng(V).standard_normal((m, n))
     H.compress(W, H.HiNMConfig(V, 2, 4, 0.5), synth.random_sigma_o(m, V + 1), saliency=S)
+# the compressor's other tile-sort paths: n > 4096 (1024-thread CTAs, 8192 buckets) and tie-heavy
+# scores (two magnitudes -> buckets beyond the limit -> bitonic network)
+W = torch.as_tensor(synth.randn_bf16((64, 4608), 7)).to("cuda", torch.bfloat16)
+H.compress(W, H.HiNMConfig(64, 2, 4, 0.5), synth.random_sigma_o(64, 8))
+Wt = torch.where(torch.rand(128, 1024, device="cuda") < 0.5, 1.0, 2.0).to(torch.bfloat16)
+Wt[:, ::2] = 1.0
+H.compress(Wt, H.HiNMConfig(64, 2, 4, 0.5), synth.random_sigma_o(128, 9))
 # gyro search kernels on a small instance (OCP + k-means + ICP)
 Wg = synth.randn_bf16((128, 64), 3).astype(np.float64)
 P.gyro_permute(Wg, H.HiNMConfig(32, 2, 4, 0.5, ocp_max_iters=2, icp_max_iters=2, seed=1))
