@@ -78,7 +78,7 @@ enum { HINM_UNPACK_REFERENCE_VIEW = 0, HINM_UNPACK_OPERAND_IMAGE = 1 };
  *   a_vals                 compressed A (V x kp_t/2 per tile) in UMMA K-major core-matrix order
  *   a_meta                 tcgen05 2:4 metadata, V lanes x 16 B per 128-K block
  */
-typedef struct {
+typedef struct hinm_pack_s {
   int32_t m, n, V, N, M, T;
   int64_t total_keep;
   int32_t* tile_ptr;
@@ -93,6 +93,15 @@ typedef struct {
   int32_t* gidx;
   uint16_t* a_vals;
   uint32_t* a_meta;
+  /* Union-group image (hinm_group_plan / hinm_group_build; NULL / 0 when not built):
+   *   group   a pseudo pack of 128-row tiles used by hinm_spmm_bf16 instead of this pack's image
+   *           when it is the faster of the two for the call's token count
+   * and, in that pseudo pack:
+   *   pair    1: tiles 2u, 2u+1 are the two halves of 256-row group u (the CTA-pair kernel)
+   *   rows    output rows (the original m; pseudo rows >= rows are zero padding) */
+  struct hinm_pack_s* group;
+  int32_t pair;
+  int32_t rows;
 } hinm_pack_t;
 
 const char* hinm_version(void);
@@ -160,7 +169,9 @@ int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* saliency, i
  * HiNM SpMM on tcgen05 (north-star subsystems 2+3): Y = W_hinm @ X, bf16 in, fp32 accumulate
  * in TMEM, bf16 out.  Rows of Y in sigma_o order (HINM_ORDER_SIGMA, == hinm_spmm) or original
  * channel order (HINM_ORDER_ORIGINAL, == restore_row_order(hinm_spmm)).  Requires the operand
- * image, B % 8 == 0, ldx % 8 == 0, ldy % 8 == 0, 16-byte aligned X/Y.  Async.
+ * image, B % 8 == 0, ldx % 8 == 0, ldy % 8 == 0, 16-byte aligned X/Y.  With a union-group image
+ * attached (pack->group) the faster image for B tokens runs; a union-group pseudo pack passed
+ * directly always runs on the CTA-pair kernel.  Async.
  */
 int hinm_spmm_bf16(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
                    uint16_t* Y, int64_t ldy, int out_order, void* stream);
@@ -201,6 +212,29 @@ int hinm_spmm_simt_f32(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, 
  */
 int hinm_unpack_to_reference(const hinm_pack_t* pack, int source, int32_t* tile_ptr, int32_t* vec_idx,
                              uint8_t* nm_pos, uint16_t* kept, int32_t* sigma_o, void* stream);
+
+/*
+ * Union-group operand image (2:4, V in {32, 64}; SURVEY §8(a) a10/a13 -- a B200 layout of the same
+ * HiNMEncoding, no reference analogue).  G = 256 / V consecutive tiles (256 rows in sigma_o order)
+ * share one gather list: the union of their kept vectors, cut into 4-slot chunks in which every row
+ * has at most two nonzeros, i.e. a 2:4 matrix of 256 rows that one CTA pair computes with
+ * tcgen05.mma.sp.cta_group::2 (half the gathered bytes per flop of the per-tile image at V = 64).
+ *   hinm_group_workspace  device workspace bytes for plan + build
+ *   hinm_group_plan       chunking (first fit of the union columns); writes the chunk count of
+ *                         each of the U = ceil(m / 256) groups to nchunks_host.  Synchronizing.
+ *   hinm_group_build      fills the caller-allocated pseudo pack `g` (V = 128, T = 2U, m = 256U,
+ *                         n = pack n, total_keep = 8 * sum(nchunks), sigma_o = the pack's, operand
+ *                         image capacities from hinm_pack_capacity) -- its reference view is the
+ *                         union layout (nm_index / kept_values per row and chunk), its operand image
+ *                         is built as for V = 128; sets g->pair = 1, g->rows = m.  Synchronizing
+ *                         (HINM_ERR_INVARIANT if a chunk would hold three nonzeros of one row).
+ * Link the result with pack->group = g; hinm_spmm_bf16 then picks the faster image per call.
+ */
+int hinm_group_workspace(const hinm_pack_t* pack, size_t* bytes);
+int hinm_group_plan(const hinm_pack_t* pack, void* workspace, size_t workspace_bytes, int32_t* nchunks_host,
+                    void* stream);
+int hinm_group_build(const hinm_pack_t* pack, void* workspace, size_t workspace_bytes, hinm_pack_t* g,
+                     void* stream);
 
 /* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
 int hinm_last_launch_count(void);

@@ -37,18 +37,20 @@ HINM_UNPACK_REFERENCE_VIEW, HINM_UNPACK_OPERAND_IMAGE = 0, 1
 
 
 class PackStruct(ctypes.Structure):
-    """Mirror of hinm_pack_t."""
+    """Mirror of hinm_pack_t (``group`` points at the union-group pseudo pack, if built)."""
 
-    _fields_ = [
-        ("m", ctypes.c_int32), ("n", ctypes.c_int32), ("V", ctypes.c_int32),
-        ("N", ctypes.c_int32), ("M", ctypes.c_int32), ("T", ctypes.c_int32),
-        ("total_keep", c_i64),
-        ("tile_ptr", c_vp), ("vec_idx", c_vp), ("nm_pos", c_vp), ("kept_bf16", c_vp),
-        ("sigma_o", c_vp),
-        ("kpad_cap", c_i64), ("meta_words_cap", c_i64),
-        ("tile_kofs", c_vp), ("tile_eofs", c_vp), ("gidx", c_vp), ("a_vals", c_vp),
-        ("a_meta", c_vp),
-    ]
+
+PackStruct._fields_ = [
+    ("m", ctypes.c_int32), ("n", ctypes.c_int32), ("V", ctypes.c_int32),
+    ("N", ctypes.c_int32), ("M", ctypes.c_int32), ("T", ctypes.c_int32),
+    ("total_keep", c_i64),
+    ("tile_ptr", c_vp), ("vec_idx", c_vp), ("nm_pos", c_vp), ("kept_bf16", c_vp),
+    ("sigma_o", c_vp),
+    ("kpad_cap", c_i64), ("meta_words_cap", c_i64),
+    ("tile_kofs", c_vp), ("tile_eofs", c_vp), ("gidx", c_vp), ("a_vals", c_vp),
+    ("a_meta", c_vp),
+    ("group", ctypes.POINTER(PackStruct)), ("pair", ctypes.c_int32), ("rows", ctypes.c_int32),
+]
 
 
 class ChainStep(ctypes.Structure):
@@ -86,6 +88,9 @@ _SIGNATURES = {
     "hinm_lex_assignment": ([c_vp, c_int, c_vp], c_int),
     "hinm_ocp_workspace": ([c_int, c_int, c_int, ctypes.POINTER(c_size)], c_int),
     "hinm_sq_dists": ([c_vp, c_int, c_vp, c_int, c_int, c_vp, c_vp], c_int),
+    "hinm_group_workspace": ([ctypes.POINTER(PackStruct), ctypes.POINTER(c_size)], c_int),
+    "hinm_group_plan": ([ctypes.POINTER(PackStruct), c_vp, c_size, c_vp, c_vp], c_int),
+    "hinm_group_build": ([ctypes.POINTER(PackStruct), c_vp, c_size, ctypes.POINTER(PackStruct), c_vp], c_int),
     "hinm_ocp_costs": ([c_vp, c_vp, c_int, c_int, c_int, c_i64, ctypes.c_double, c_vp, c_vp, c_size, c_vp],
                        c_int),
 }

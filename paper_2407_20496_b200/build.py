@@ -28,10 +28,12 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libhinm_b200.so")
 EXP_LIB = os.path.join(ROOT, "scripts", "libhinm_b200_exp.so")
 SOURCES = ["compress.cu", "spmm_sm100.cu", "spmm_simt.cu", "chain_host.cu", "capi.cu",
-           "icp.cu", "assignment.cu", "unpack.cu", "ocp.cu", "kmeans.cu"]
+           "icp.cu", "assignment.cu", "unpack.cu", "ocp.cu", "kmeans.cu", "group.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
+# experiments build only: extra defines (e.g. HINM_EXP_FLAGS="-DHINM_PAIR_STAGES=5")
+EXP_FLAGS = os.environ.get("HINM_EXP_FLAGS", "").split()
 
 
 def _deps_mtime() -> float:
@@ -42,7 +44,7 @@ def _deps_mtime() -> float:
 
 def _compile(src: str, experiments: bool = False) -> str:
     obj = os.path.join(BUILD, src.replace(".cu", "_exp.o" if experiments else ".o"))
-    extra = ["-DHINM_EXPERIMENTS"] if experiments else []
+    extra = ["-DHINM_EXPERIMENTS", *EXP_FLAGS] if experiments else []
     cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

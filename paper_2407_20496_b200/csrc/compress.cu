@@ -1953,18 +1953,20 @@ extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
   HINM_LAUNCH_CHECK();
   HINM_CUDA_TRY(cudaMemsetAsync(p->a_vals, 0, (size_t)acap * 2, stream));
   const int64_t groups = p->total_keep / 4;
+  // largest k_t: n (a tile's vectors), 4n for a union-group pseudo pack (hinm_group_build)
+  const int64_t kmax = p->pair ? 4 * (int64_t)p->n : p->n;
   if (groups > 0) {
-    // one thread per (chunk of 4 groups, row); a tile has at most ceil(n / 16) chunks
-    dim3 gv((unsigned)ceil_div(ceil_div(p->n, 16) * V, 256), T);
+    // one thread per (chunk of 4 groups, row); a tile has at most ceil(kmax / 16) chunks
+    dim3 gv((unsigned)ceil_div(ceil_div(kmax, 16) * V, 256), T);
     k_pack_vals16<<<gv, 256, 0, stream>>>(p->tile_ptr, p->tile_kofs, p->kept_bf16, V, p->a_vals);
     HINM_LAUNCH_CHECK();
   }
   // a tile has at most ceil(round_up(n, 64) / 128) metadata blocks
-  const int64_t max_blocks = ceil_div(round_up(p->n, 64), 128);
+  const int64_t max_blocks = ceil_div(round_up(kmax, 64), 128);
   dim3 gm((unsigned)ceil_div(max_blocks * V * 4, 256), T);
   k_pack_meta<<<gm, 256, 0, stream>>>(p->tile_ptr, p->tile_eofs, p->nm_pos, V, T, p->a_meta);
   HINM_LAUNCH_CHECK();
-  dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p->n, 256), 64)), T);
+  dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(kmax, 256), 64)), T);
   k_pack_gidx<<<gg, 256, 0, stream>>>(p->tile_ptr, p->tile_kofs, p->vec_idx, p->gidx);
   HINM_LAUNCH_CHECK();
   return HINM_OK;

@@ -27,6 +27,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cmath>
 #include <initializer_list>
 #include <mutex>
 #include <vector>
@@ -45,7 +47,12 @@ constexpr int MAX_ASTAGES = 12;                // compressed-A / metadata ring (
 // per-stage cost in every producer warp (barrier wait + arrive), so 128-row stages
 // (16 warps x 8 rows) stream markedly faster than 64-row ones (scripts/l2_ring.cu on B200:
 // 20.4 vs 16.6 TB/s).
-__host__ __device__ constexpr int b_stages(int KS, int BNT) { return (KS == 128 ? 3 : 5) * (256 / BNT); }
+#ifndef HINM_PAIR_STAGES
+#define HINM_PAIR_STAGES 4
+#endif
+__host__ __device__ constexpr int b_stages(int KS, int BNT, bool pair = false) {
+  return pair ? (KS == 128 ? HINM_PAIR_STAGES : 2 * HINM_PAIR_STAGES) : (KS == 128 ? 3 : 5) * (256 / BNT);
+}
 __host__ __device__ constexpr int b_stage_bytes(int KS, int BNT) { return KS * BNT * 2; }
 constexpr int MAX_XSTAGES = 10;
 constexpr int E_STAGE = 128 * 16;              // 128 lanes x 16 B metadata image per stage slot
@@ -68,6 +75,8 @@ struct Params {
   int V;
   int units;
   int out_order;
+  int rows;           // output rows (pseudo rows >= rows of a union-group pack are padding)
+  int tdiv;           // unit -> (tile, token block) divisor: T, or T / 2 groups on the CTA-pair path
   int y_align32;      // Y rows 32-byte aligned: 256-bit stores
   uint32_t xpitch;    // bytes between consecutive K-rows (channels) of X
   int64_t xblk;       // bytes between consecutive BNT-token blocks of X
@@ -81,18 +90,18 @@ struct SmemLayout {
 // cp.async gather under load, and with a shared barrier they held every X stage hostage
 // (scripts/l2_ring.cu).  One A stage covers one X stage (KS logical K: V*KS bytes of compressed
 // values + one metadata slot); depth = whatever fits next to the X ring.
-__host__ __device__ inline SmemLayout smem_layout(int V, int KS, bool m64, int BNT) {
+__host__ __device__ inline SmemLayout smem_layout(int V, int KS, bool m64, int BNT, bool pair = false) {
   SmemLayout L;
-  const uint32_t slack = m64 ? 0 : 4096;       // M=128 descriptor over-read past V rows
-  const uint32_t budget = 227 * 1024 - 1024 - 512 - slack;
+  const uint32_t slack = m64 || pair ? 0 : 4096;   // M=128 descriptor over-read past V rows
+  const uint32_t budget = 227 * 1024 - 1024 - 512 - 128 - slack;
   const uint32_t per = V * KS + E_STAGE;
-  const uint32_t xring = b_stages(KS, BNT) * b_stage_bytes(KS, BNT);
+  const uint32_t xring = b_stages(KS, BNT, pair) * b_stage_bytes(KS, BNT);
   const uint32_t fit = (budget - xring) / per;
   L.ast = fit < (uint32_t)MAX_ASTAGES ? fit : MAX_ASTAGES;
   L.a = xring;
   L.e = L.a + L.ast * V * KS + slack;
   L.bar = L.e + L.ast * E_STAGE;
-  L.tmem = L.bar + (2 * MAX_XSTAGES + 2 * MAX_ASTAGES + 4) * 8;
+  L.tmem = L.bar + (3 * MAX_XSTAGES + 2 * MAX_ASTAGES + 4) * 8;
   L.total = L.tmem + 16 + 1024;                // + alignment slack for the 1 KB base
   return L;
 }
@@ -193,6 +202,43 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ---- CTA pair (cluster of 2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// Relaxed: a release arrive compiles to MEMBAR.GPU (+ the waiter's acquire.cluster to CCTL.IVALL),
+// ~1-2 k cycles on the per-stage critical path (ncu source view, profiles/r03_pair.txt).  What the
+// leader needs is already established before the arrive: the peer's cp.async / bulk writes have
+// completed (its local full barrier), its TMEM loads have completed (tcgen05.wait::ld).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Per-stage event trace of CTA pair 0 (experiments build with -DHINM_TRACE; scripts/pair_trace.py):
+// clock64 of each role's barrier completions, per running stage index; slot 10 = the two CTAs'
+// clocks right after the start-up cluster barrier (offset calibration).
+#ifdef HINM_TRACE
+__device__ unsigned long long g_trace[11][1024];
+#define TRACE(ev, i)                                                                     \
+  do {                                                                                   \
+    if (blockIdx.x < 2 && (i) < 1024) g_trace[ev][i] = (unsigned long long)clock64();    \
+  } while (0)
+#else
+#define TRACE(ev, i) \
+  do {               \
+  } while (0)
+#endif
+
 // parity to wait on for the n-th (0-based) use of a buffer guarded by an "empty" barrier
 __device__ __forceinline__ uint32_t phase_acc_empty_parity(uint32_t n) { return (n & 1) ^ 1; }
 
@@ -206,6 +252,17 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
+}
+// CTA pair: the leader's commit arrives on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void tc_commit_x(uint32_t bar) {
+  if (PAIR) tc_commit_pair(bar); else tc_commit(bar);
 }
 
 // UMMA shared-memory matrix descriptor (tcgen05 format, version 1).
@@ -231,19 +288,33 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+template <bool PAIR = false>
 __device__ __forceinline__ void mma_sp(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
                                        uint32_t idesc, uint32_t tmem_e, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t"
-      "}\n" ::"r"(tmem_d),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(tmem_e)
-      : "memory");
+  if (PAIR)  // CTA pair, M = 256: each CTA's 128 rows of A x the pair's B (N split over the CTAs)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t"
+        "}\n" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(tmem_e)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t"
+        "}\n" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(tmem_e)
+        : "memory");
 }
 
+template <bool PAIR = false>
 __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+  if (PAIR)  // both CTAs: own shared memory -> own TMEM (scripts/probe_2sm.cu)
+    asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+  else
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
 // 16 lanes x (32 + 32) columns: thread l < 16 gets lane l, columns c..c+31; thread l >= 16 gets
@@ -292,6 +363,15 @@ constexpr int AE_WARP = 9;
 // fast as 8 warps (LLaMA up 0.741 vs 0.740 ms): under a running MMA the gather is capped by the
 // SM's L2->SMEM fill rate, not by issuing warps (scripts/mma_gather_contention.cu).
 __host__ __device__ constexpr int gather_warp0(int GW) { return GW == 8 ? 10 : 12; }
+// CTA pair, 8 gather warps: the gather warps avoid the MMA warp's SM sub-partition (warp % 4 == 0).
+// On the leader the issue of tcgen05.mma.cta_group::2 / commit held back the gather warps that share
+// its sub-partition and, through the barrier, the whole stage: the leader's stage fill took ~700
+// cycles longer than the peer's, also with the gather itself disabled (scripts/pair_trace.py).
+// Warps 12 and 16 stay idle.
+__host__ __device__ constexpr bool gather_spread(int GW, bool pair) { return pair && GW == 8; }
+__host__ __device__ constexpr int kernel_warps(int GW, bool pair) {
+  return gather_spread(GW, pair) ? 20 : gather_warp0(GW) + GW;
+}
 constexpr int GATHER_REGS = 56, EPI_REGS = 104;
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
@@ -311,14 +391,16 @@ struct UnitParams {
   int t, nb, k0, kp, e0;
 };
 
-__device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
+// CTA pair: unit u = (group u % tdiv, token block u / tdiv); CTA r works on pseudo tile 2g + r.
+template <bool PAIR = false>
+__device__ __forceinline__ UnitParams unit_params(const Params& p, int u, int crank = 0) {
   UnitParams q;
   if (u >= p.units) {
     q.t = q.nb = q.k0 = q.kp = q.e0 = 0;
     return q;
   }
-  q.t = u % p.T;
-  q.nb = u / p.T;
+  q.t = PAIR ? 2 * (u % p.tdiv) + crank : u % p.T;
+  q.nb = u / p.tdiv;
   q.k0 = __ldg(p.tile_kofs + q.t);
   q.kp = __ldg(p.tile_kofs + q.t + 1) - q.k0;
   q.e0 = __ldg(p.tile_eofs + q.t);
@@ -335,28 +417,43 @@ __device__ __forceinline__ UnitParams unit_params(const Params& p, int u) {
 // accumulator row 16q+l sits in TMEM lane 32q+l and its metadata where M=128 row 32q+l would
 // (lanes 32q+0..15) -- measured with scripts/probe_sparse_meta.cu, which also shows that an
 // M=64 accumulator at lane offset 16 faults (misaligned address), so one accumulator is used.
-template <int KS, int GW, int DBG = 0, bool M64 = false, int BNT = 256>
-__global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
+// PAIR (union-group pseudo packs, hinm_group_build): a cluster of two CTAs computes one 256-row
+// group with tcgen05.mma.sp.cta_group::2 (M = 256, N = 256).  CTA r holds pseudo tile 2g + r (128
+// rows of A, V = 128 image) and gathers tokens [256 nb + 128 r, +128) of the shared K-rows
+// (BNT = 128 per CTA); its TMEM accumulator is its 128 rows x all 256 tokens.  The leader (rank
+// 0) issues the MMAs once both CTAs' stages have landed: the peer's MMA warp relays each stage
+// (local full + A barriers) to the leader's pfull barrier; the leader's commits multicast to the
+// empty / accumulator barriers of both CTAs; the peer's epilogue releases the accumulator to the
+// leader's acc_empty barrier.
+template <int KS, int GW, int DBG = 0, bool M64 = false, int BNT = 256, bool PAIR = false>
+__global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
     k_hinm_spmm(const uint16_t* __restrict__ X, int64_t ldx, Params p) {
   constexpr int GATHER_WARP0 = gather_warp0(GW);
   constexpr bool REBALANCE = GATHER_WARP0 % 4 == 0 && GW % 4 == 0;
-  constexpr int NT = 32 * (GATHER_WARP0 + GW);
-  constexpr int STAGES = b_stages(KS, BNT), B_STAGE = b_stage_bytes(KS, BNT);
+  constexpr int NT = 32 * kernel_warps(GW, PAIR);
+  constexpr bool SPREAD = gather_spread(GW, PAIR);
+  constexpr int STAGES = b_stages(KS, BNT, PAIR), B_STAGE = b_stage_bytes(KS, BNT);
   constexpr int NCHUNK = BNT / 64;            // 64-token SWIZZLE_128B chunks of a stage
-  constexpr int NACC = BNT == 128 ? 2 : 1;    // accumulators (TMEM columns 0 and 128)
+  constexpr int NACC = BNT == 128 && !PAIR ? 2 : 1;  // accumulators (TMEM columns 0 and 128)
+  constexpr int NTOK = PAIR ? 256 : BNT;      // tokens per unit (accumulator columns)
   static_assert(STAGES <= MAX_XSTAGES, "X ring");
+  static_assert(!PAIR || (BNT == 128 && !M64), "CTA pair: 128 tokens per CTA, M = 256");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const SmemLayout L = smem_layout(p.V, KS, M64, BNT);
+  const SmemLayout L = smem_layout(p.V, KS, M64, BNT, PAIR);
   const int V = p.V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const int ublk = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;    // first unit of this CTA (pair)
+  const int ugrid = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;     // unit stride
   const uint32_t sB = base, sA = base + L.a, sE = base + L.e;
   const uint32_t bar_full = base + L.bar, bar_empty = bar_full + STAGES * 8;
   const uint32_t bar_afull = bar_empty + STAGES * 8, bar_aempty = bar_afull + MAX_ASTAGES * 8;
   const uint32_t bar_acc_full = bar_aempty + MAX_ASTAGES * 8;   // [NACC]
   const uint32_t bar_acc_empty = bar_acc_full + 16;             // [NACC]
+  const uint32_t bar_pfull = bar_acc_empty + 16;                // [STAGES] (PAIR, leader)
   const int AST = (int)L.ast;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + L.tmem);
   // TMEM lane quadrants that hold real rows; two epilogue warps (column halves) per quadrant
@@ -384,19 +481,30 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(bar_acc_full + 8 * a, 1);
-      mbar_init(bar_acc_empty + 8 * a, n_epi_warps);
+      mbar_init(bar_acc_empty + 8 * a, n_epi_warps * (PAIR ? 2 : 1));  // PAIR: both CTAs' epilogues
     }
+    if (PAIR)
+      for (int s = 0; s < STAGES; ++s) mbar_init(bar_pfull + 8 * s, 1);  // one relay per peer stage
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == MMA_WARP) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // barrier inits visible to the peer before any remote arrive
+  if (threadIdx.x == 0) TRACE(10, crank);
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const int T = p.T;
@@ -412,17 +520,20 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     // warp-uniform loop; one elected lane issues the bulk copies (see the MMA issuer note)
     int aslot = 0;
     uint32_t aphase = 0;
-    UnitParams nxt = unit_params(p, blockIdx.x);
+    UnitParams nxt = unit_params<PAIR>(p, ublk, crank);
+    int a_count = 0;
     const uint32_t a_slot = V * KS;
     const uint64_t pol_a = l2_policy_evict_last();
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int u = ublk; u < p.units; u += ugrid) {
       const UnitParams cur = nxt;
-      nxt = unit_params(p, u + gridDim.x);
+      nxt = unit_params<PAIR>(p, u + ugrid, crank);
       const int nst = cur.kp / BK;                         // 64-K steps of the unit
       const uint16_t* asrc = p.a_vals + (int64_t)cur.k0 * V / 2;
       const uint32_t* esrc0 = p.a_meta + (int64_t)cur.e0 * V * 4;
       for (int s = 0; s < nst; s += KS / BK) {             // one A stage per X stage
         mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
+        if (lane == 0) TRACE(7 + crank, a_count);
+        ++a_count;
         const uint32_t fb = bar_afull + 8 * aslot;
         if (DBG == 4 || (DBG == 7 && (cur.nb & 1))) {  // experiments: no A / metadata loads
           // (DBG 7: on every other token block, i.e. the A image read once per 512 tokens)
@@ -446,7 +557,12 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
     }
-  } else if (warp >= GATHER_WARP0) {
+    if (PAIR)  // producer tail: the leader's last commits have landed before this CTA may exit
+      for (int i = 0; i < AST; ++i) {
+        mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
+        if (++aslot == AST) { aslot = 0; aphase ^= 1; }
+      }
+  } else if (warp >= GATHER_WARP0 && !(SPREAD && (warp & 3) == 0)) {
     // ============================================================ gather producers
     if (REBALANCE) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(GATHER_REGS));
     // Flattened stream over (unit, X stage) with the gather indices of stage i+PF loaded while
@@ -454,22 +570,24 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     // issue loop is kept to ~4 instructions per 512-byte row: warp gw owns the K-rows
     // r = gw + GW*i of every stage, lane = 16-byte chunk of the row.  The last stage of a unit
     // may be partial (kp is a multiple of 64, KS may be 128).
-    const int gw = warp - GATHER_WARP0;
+    const int gw = SPREAD ? warp - 10 - (warp > 12) - (warp > 16) : warp - GATHER_WARP0;
     constexpr int PF = 8;
     constexpr int RPW = KS / GW;  // K-rows per warp per stage
     static_assert(KS % GW == 0 && GW >= 8 && RPW <= 32, "gather producers: GW | KS, GW >= 8");
-    const int dt = gridDim.x % T, dnb = gridDim.x / T;
+    const int TD = p.tdiv;  // tiles (groups on the CTA-pair path) per token block
+    const int dt = ugrid % TD, dnb = ugrid / TD;
     // prefetch cursor: unit (pt, pnb) with running index pu, stage ps, kp of the unit
-    int pu = blockIdx.x, pt = blockIdx.x % T, pnb = blockIdx.x / T, ps = 0, pk0 = 0, pkp = 0;
+    int pu = ublk, pt = ublk % TD, pnb = ublk / TD, ps = 0, pk0 = 0, pkp = 0;
     auto next_unit = [&]() {  // advance to the next unit with work
       while (pu < p.units) {
-        pk0 = __ldg(p.tile_kofs + pt);
-        pkp = __ldg(p.tile_kofs + pt + 1) - pk0;
+        const int tt = PAIR ? 2 * pt + (int)crank : pt;
+        pk0 = __ldg(p.tile_kofs + tt);
+        pkp = __ldg(p.tile_kofs + tt + 1) - pk0;
         if (pkp > 0) break;
-        pu += gridDim.x;
+        pu += ugrid;
         pt += dt;
         pnb += dnb;
-        if (pt >= T) { pt -= T; ++pnb; }
+        if (pt >= TD) { pt -= TD; ++pnb; }
       }
       ps = 0;
     };
@@ -484,17 +602,17 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         if (j != slot) continue;
         r_ok[j] = pu < p.units;
         if (!r_ok[j]) return;
-        r_col[j] = pnb * BNT;
+        r_col[j] = PAIR ? pnb * 256 + (int)crank * 128 : pnb * BNT;
         const int n = min(KS, pkp - ps * KS);
         r_n[j] = n;
         const int* gi = p.gidx + pk0 + ps * KS;
         // raw row index: it is consumed PF stages later, so the load never stalls the warp here
         r_row[j] = lane < RPW && gw + lane * GW < n ? (uint32_t)__ldg(gi + gw + lane * GW) : 0u;
         if (++ps * KS >= pkp) {
-          pu += gridDim.x;
+          pu += ugrid;
           pt += dt;
           pnb += dnb;
-          if (pt >= T) { pt -= T; ++pnb; }
+          if (pt >= TD) { pt -= TD; ++pnb; }
           next_unit();
         }
       }
@@ -508,7 +626,7 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     const uint32_t dst_lane = (lpos >> 3) * (B_STAGE / NCHUNK) + (gw + rsub * GW) * 128 +
                               (((lpos & 7) ^ (gw & 7)) << 4);
     const char* xbase = reinterpret_cast<const char*>(X);
-    int stage = 0;
+    int stage = 0, g_count = 0;
     uint32_t phase = 0;
     bool done = false;
     while (!done) {
@@ -519,10 +637,14 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         // scarce resource, ncu source view); rows < 64 always exist, the rest only in full stages
         const int tok = r_col[j] + lpos * 8;
         const uint32_t src_bytes = tok < p.B ? 16u : 0u;
-        const char* xs = xbase + (src_bytes ? (int64_t)(r_col[j] / BNT) * p.xblk + lpos * 16 : 0);
+        const char* xs = xbase + (src_bytes ? (PAIR ? (int64_t)r_col[j] * 2 : (int64_t)(r_col[j] / BNT) * p.xblk) +
+                                                  lpos * 16
+                                            : 0);
         const uint32_t my_row = r_row[j];
         const bool full = r_n[j] == KS;
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        if (gw == 0 && lane == 0) TRACE(5 + crank, g_count);
+        ++g_count;
         const uint32_t dst0 = sB + stage * B_STAGE + dst_lane;
 #pragma unroll
         for (int k = 0; k < RPW / RPI; ++k) {
@@ -536,28 +658,59 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
         prefetch(j);
       }
     }
+    if (PAIR)  // producer tail (see the A producer)
+      for (int i = 0; i < STAGES; ++i) {
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+  } else if (PAIR && warp == MMA_WARP && crank != 0) {
+    // ============================================================ peer relay (CTA pair, rank 1)
+    // The peer's X stage and A / metadata stage have landed in ITS shared memory: tell the leader,
+    // whose MMAs read them.  Same unit / stage sequence as the leader's issue loop.
+    const uint32_t rem_pfull = mapa_rank(bar_pfull, 0);
+    int stage = 0, aslot = 0, r_count = 0;
+    uint32_t phase = 0, aphase = 0;
+    UnitParams nxt = unit_params<PAIR>(p, ublk, crank);
+    for (int u = ublk; u < p.units; u += ugrid) {
+      const int kp = nxt.kp;
+      nxt = unit_params<PAIR>(p, u + ugrid, crank);
+      if (kp == 0) continue;
+      for (int s0 = 0; s0 < kp / BK; s0 += KS / BK) {
+        mbar_wait(bar_full + 8 * stage, phase);
+        if (lane == 0) TRACE(3, r_count);
+        mbar_wait(bar_afull + 8 * aslot, aphase);
+        if (lane == 0) TRACE(4, r_count);
+        ++r_count;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (elect_one()) mbar_arrive_remote(rem_pfull + 8 * stage);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++aslot == AST) { aslot = 0; aphase ^= 1; }
+      }
+    }
   } else if (warp == MMA_WARP) {
     // ============================================================ MMA issuer
     // The whole warp runs the loop (warp-uniform control flow keeps every descriptor in uniform
     // registers); one elected lane issues the tcgen05 instructions.  A single-lane loop forced
     // R2UR conversions of every operand per MMA and measured 2.6x slower MMA issue
     // (scripts/mma_bench.cu vs mma_bench_v1.cu).
-    const uint32_t idesc = make_idesc(M64 ? 64 : 128, BNT);
+    const uint32_t idesc = make_idesc(PAIR ? 256 : M64 ? 64 : 128, NTOK);
     // descriptors at stage 0; the start-address field (16 B units, bits 0-13) is advanced by
     // adding byte offsets >> 4
     const uint64_t a_desc0 = smem_desc(sA, 128, 256, 0);
     const uint64_t b_desc0 = smem_desc(sB, B_STAGE / NCHUNK, 1024, 2);
     const uint64_t e_desc0 = smem_desc(sE, 0, 128, 0);
     const uint32_t a_step = (uint32_t)(V * KS) >> 4, a_half = (uint32_t)(32 * V) >> 4;
-    int stage = 0, aslot = 0;
+    int stage = 0, aslot = 0, m_count = 0;
     uint32_t phase = 0, aphase = 0, eslot = 0, acc_uses = 0;
-    UnitParams nxt = unit_params(p, blockIdx.x);
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    UnitParams nxt = unit_params<PAIR>(p, ublk, crank);
+    for (int u = ublk; u < p.units; u += ugrid) {
       const int kp = nxt.kp;
-      nxt = unit_params(p, u + gridDim.x);
+      nxt = unit_params<PAIR>(p, u + ugrid, crank);
       if (kp == 0) continue;
       const uint32_t acc = NACC == 2 ? (acc_uses & 1) : 0;
       mbar_wait(bar_acc_empty + 8 * acc, phase_acc_empty_parity(acc_uses / NACC));
+      if (lane == 0) TRACE(9, acc_uses);
       ++acc_uses;
       tc_fence_after();
       const uint32_t dtm = tmem + acc * BNT;
@@ -569,32 +722,37 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
       for (int s0 = 0; s0 < nst; s0 += SUB) {
         const bool two = SUB == 2 && s0 + 1 < nst;
         mbar_wait(bar_full + 8 * stage, phase);
+        if (lane == 0) TRACE(0, m_count);
         mbar_wait(bar_afull + 8 * aslot, aphase);
+        if (lane == 0) TRACE(1, m_count);
+        if (PAIR) mbar_wait(bar_pfull + 8 * stage, phase);  // the peer's stage too (relayed)
+        if (lane == 0) TRACE(2, m_count);
+        ++m_count;
         tc_fence_after();
         if (elect_one()) {
           if ((s0 & 1) == 0) {  // metadata of the 128-K block starting at this step
             eslot = (eslot + 1) & (E_SLOTS - 1);
-            tmem_cp_128x128b(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((aslot * E_STAGE) >> 4));
+            tmem_cp_128x128b<PAIR>(tmem + E_COL + eslot * 4, e_desc0 + (uint64_t)((aslot * E_STAGE) >> 4));
           }
           const uint32_t ecol = tmem + E_COL + eslot * 4 + (s0 & 1) * 2;
           const uint64_t ad = a_desc0 + (uint64_t)(aslot * a_step);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * B_STAGE) >> 4);
           if (DBG != 1 && DBG != 4 && DBG != 5) {
-            mma_sp(dtm, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
-            mma_sp(dtm, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
+            mma_sp<PAIR>(dtm, ad, bd, idesc, ecol, s0 ? 1u : 0u);                      // id2 = 0
+            mma_sp<PAIR>(dtm, ad + a_half, bd + (4096 >> 4), idesc | 1u, ecol, 1u);   // id2 = 1
             if (two) {
-              mma_sp(dtm, ad + 2 * a_half, bd + (8192 >> 4), idesc, ecol + 2, 1u);
-              mma_sp(dtm, ad + 3 * a_half, bd + (12288 >> 4), idesc | 1u, ecol + 2, 1u);
+              mma_sp<PAIR>(dtm, ad + 2 * a_half, bd + (8192 >> 4), idesc, ecol + 2, 1u);
+              mma_sp<PAIR>(dtm, ad + 3 * a_half, bd + (12288 >> 4), idesc | 1u, ecol + 2, 1u);
             }
           }
-          tc_commit(bar_aempty + 8 * aslot);
-          tc_commit(bar_empty + 8 * stage);
+          tc_commit_x<PAIR>(bar_aempty + 8 * aslot);
+          tc_commit_x<PAIR>(bar_empty + 8 * stage);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++aslot == AST) { aslot = 0; aphase ^= 1; }
       }
-      if (elect_one()) tc_commit(bar_acc_full + 8 * acc);
+      if (elect_one()) tc_commit_x<PAIR>(bar_acc_full + 8 * acc);
       __syncwarp();
     }
   } else if (warp < EPI_WARPS) {
@@ -613,11 +771,19 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
     if (q < n_quads) {
       uint32_t ucount = 0;
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;
-      const int c_own = M64 && lane >= 16 ? BNT / 2 : 0;
-      constexpr int NCH = M64 ? BNT / 128 : BNT / 64;  // 32-column chunks per warp
+      const int c_own = M64 && lane >= 16 ? NTOK / 2 : 0;
+      constexpr int NCH = M64 ? NTOK / 128 : NTOK / 64;  // 32-column chunks per warp
       const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16) + h * NCH * 32;
+      // release of an accumulator: local, or (CTA pair, rank 1) to the leader's barrier
+      const uint32_t acc_empty_dst = PAIR && crank ? mapa_rank(bar_acc_empty, 0) : bar_acc_empty;
+      auto release = [&](uint32_t acc) {
+        if (PAIR && crank) mbar_arrive_remote(acc_empty_dst + 8 * acc);
+        else mbar_arrive(bar_acc_empty + 8 * acc);
+      };
+      // output row of this lane for a unit; -1: a padding row of a union-group pseudo pack
       auto out_row = [&](const UnitParams& u) -> int64_t {
         const int64_t prow = (int64_t)u.t * V + r;
+        if (prow >= p.rows) return -1;
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
       };
       // 32 accumulator columns (fp32 bits) -> bf16 -> 4 x 16-byte stores of one row segment
@@ -651,29 +817,42 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
           }
         }
       };
-      UnitParams nxt = unit_params(p, blockIdx.x);
-      int64_t nxt_row = blockIdx.x < p.units ? out_row(nxt) : 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      UnitParams nxt = unit_params<PAIR>(p, ublk, crank);
+      int64_t nxt_row = ublk < p.units ? out_row(nxt) : 0;
+      for (int u = ublk; u < p.units; u += ugrid) {
         const UnitParams cur = nxt;
         const int64_t orow = nxt_row;
-        nxt = unit_params(p, u + gridDim.x);
-        if (u + (int)gridDim.x < p.units) nxt_row = out_row(nxt);
-        uint16_t* yrow = p.Y + orow * p.ldy;
-        const int col_base = cur.nb * BNT + c_own + h * NCH * 32;
+        nxt = unit_params<PAIR>(p, u + ugrid, crank);
+        if (u + ugrid < p.units) nxt_row = out_row(nxt);
+        const bool live = orow >= 0;
+        uint16_t* yrow = p.Y + (live ? orow : 0) * p.ldy;
+        const int col_base = cur.nb * NTOK + c_own + h * NCH * 32;
         if (cur.kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
           for (int c = 0; c < NCH * 4; ++c)
-            if (col_base + c * 8 < p.B)
+            if (live && col_base + c * 8 < p.B)
               *reinterpret_cast<uint4*>(yrow + col_base + c * 8) = make_uint4(0, 0, 0, 0);
           continue;
         }
         const uint32_t acc = NACC == 2 ? (ucount & 1) : 0;
+#ifdef HINM_EPI_SLEEP
+        {  // experiment: idle epilogue warps back off instead of spinning on the accumulator barrier
+          uint32_t ok = 0;
+          while (true) {
+            asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(ok) : "r"(bar_acc_full + 8 * acc), "r"((ucount / NACC) & 1) : "memory");
+            if (ok) break;
+            __nanosleep(HINM_EPI_SLEEP);
+          }
+        }
+#else
         mbar_wait(bar_acc_full + 8 * acc, (ucount / NACC) & 1);
+#endif
         ++ucount;
         tc_fence_after();
         const uint32_t t_acc = t_row + acc * BNT;
         if (DBG == 3) {  // experiment: release at once, no drain / stores
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
+          if (lane == 0) release(acc);
           continue;
         }
         uint32_t v0[32], v1[32];
@@ -681,8 +860,8 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
           tmem_ld_16x32bx2_x32<true, BNT / 2>(t_acc, v0);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
-          store32(yrow, col_base, v0);
+          if (lane == 0) release(acc);
+          if (live) store32(yrow, col_base, v0);
           continue;
         }
         // chunks are loaded in pairs (two tcgen05.ld in flight, one wait); the accumulator is
@@ -690,8 +869,8 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
 #pragma unroll 1
         for (int c = 0; c < NCH; c += 2) {
           if (M64) {
-            tmem_ld_16x32bx2_x32<false, BNT / 2>(t_acc + c * 32, v0);
-            tmem_ld_16x32bx2_x32<false, BNT / 2>(t_acc + c * 32 + 32, v1);
+            tmem_ld_16x32bx2_x32<false, NTOK / 2>(t_acc + c * 32, v0);
+            tmem_ld_16x32bx2_x32<false, NTOK / 2>(t_acc + c * 32 + 32, v1);
           } else {
             tmem_ld_32x32b_x32<false>(t_acc + c * 32, v0);
             tmem_ld_32x32b_x32<false>(t_acc + c * 32 + 32, v1);
@@ -700,19 +879,25 @@ __global__ void __launch_bounds__(32 * (gather_warp0(GW) + GW), 1)
           if (c + 2 == NCH) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_acc_empty + 8 * acc);
+            if (lane == 0) release(acc);
           }
-          store32(yrow, col_base + c * 32, v0);
-          store32(yrow, col_base + c * 32 + 32, v1);
+          if (live) {
+            store32(yrow, col_base + c * 32, v0);
+            store32(yrow, col_base + c * 32 + 32, v1);
+          }
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's remote arrivals and TMEM reads are done
   if (warp == MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -751,6 +936,103 @@ cudaError_t ensure_smem(const void* fn, int /*dev*/, int bytes) { return hinm::s
 
 extern "C" int hinm_last_launch_count(void) { return g_last_launches; }
 
+#ifdef HINM_TRACE
+// experiments: copy the pair-0 event trace (11 x 1024 clock64 values) to host memory
+extern "C" int hinm_exp_trace(unsigned long long* host) {
+  HINM_CUDA_TRY(cudaDeviceSynchronize());
+  HINM_CUDA_TRY(cudaMemcpyFromSymbol(host, hinm::sm100::g_trace, sizeof(unsigned long long) * 11 * 1024));
+  return HINM_OK;
+}
+#endif
+
+namespace {
+
+// The union-group pseudo pack on the CTA-pair kernel (hinm_group_build; spmm_sm100.cu PAIR).
+int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint16_t* Y, int64_t ldy,
+              int out_order, int y_align32, cudaStream_t st) {
+  using namespace hinm::sm100;
+  Params prm;
+  prm.tile_kofs = g->tile_kofs;
+  prm.tile_eofs = g->tile_eofs;
+  prm.gidx = g->gidx;
+  prm.a_vals = g->a_vals;
+  prm.a_meta = g->a_meta;
+  prm.sigma_o = g->sigma_o;
+  prm.Y = Y;
+  prm.ldy = ldy;
+  prm.B = B;
+  prm.T = g->T;
+  prm.V = 128;
+  prm.out_order = out_order;
+  prm.rows = g->rows;
+  prm.tdiv = g->T / 2;
+  prm.y_align32 = y_align32;
+  prm.units = ((B + 255) / 256) * prm.tdiv;
+  prm.xpitch = (uint32_t)(ldx * 2);
+  prm.xblk = 256 * 2;
+  const int dev = current_device();
+  const int pairs = std::min(prm.units, sm_count(dev) / 2);
+  // HINM_PAIR_KS = 64 | 128 (K-rows per X stage), HINM_PAIR_GW = 8 | 16 (gather warps)
+  static const int pks = [] { const char* e = getenv("HINM_PAIR_KS"); return e && !strcmp(e, "64") ? 64 : 128; }();
+  static const int pgw = [] { const char* e = getenv("HINM_PAIR_GW"); return e && !strcmp(e, "16") ? 16 : 8; }();
+  const int KS = pks, GW = pgw;
+  auto kern = KS == 64 ? (GW == 16 ? k_hinm_spmm<64, 16, 0, false, 128, true> : k_hinm_spmm<64, 8, 0, false, 128, true>)
+                       : (GW == 16 ? k_hinm_spmm<128, 16, 0, false, 128, true> : k_hinm_spmm<128, 8, 0, false, 128, true>);
+#ifdef HINM_EXPERIMENTS
+  // timing-only: HINM_PAIR_DBG = 1 (no MMAs) | 2 (no gather) | 3 (no epilogue); results are garbage
+  if (const char* e = getenv("HINM_PAIR_DBG")) {
+    if (e[0] == '1') kern = k_hinm_spmm<128, 8, 1, false, 128, true>;
+    if (e[0] == '2') kern = k_hinm_spmm<128, 8, 2, false, 128, true>;
+    if (e[0] == '3') kern = k_hinm_spmm<128, 8, 3, false, 128, true>;
+  }
+#endif
+  const SmemLayout L = smem_layout(128, KS, false, 128, true);
+  HINM_CUDA_TRY(ensure_smem((const void*)kern, dev, (int)L.total));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(32 * kernel_warps(GW, true));
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HINM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, X, ldx, prm));
+  HINM_LAUNCH_CHECK();
+  g_last_launches = 1;
+  return HINM_OK;
+}
+
+// Per-call choice between a pack's per-tile image and its union-group image: modelled SM time =
+// waves x K-steps x cycles per 32-K step (per-tile V <= 64 on M = 64: ~290; CTA pair: ~200 --
+// measured fill rates, profiles/r03_pair.txt).  Few units (short token counts) keep the per-tile
+// image: it has twice the units and half the K per unit.  HINM_GROUPS = 0 | 1 forces.
+bool choose_group(const hinm_pack_t* pk, int B, int sms) {
+  const hinm_pack_t* g = pk->group;
+  if (!g || !g->pair || !g->a_vals || !g->tile_kofs || g->T < 2 || pk->T < 1) return false;
+  static const int force = [] {
+    const char* e = getenv("HINM_GROUPS");
+    if (!e) return -1;
+    if (!strcmp(e, "0")) return 0;
+    if (!strcmp(e, "1")) return 1;
+    fprintf(stderr, "[hinm] invalid HINM_GROUPS=%s (0 | 1)\n", e);
+    return -2;
+  }();
+  if (force == 0 || force == -2) return false;
+  if (force == 1) return true;
+  const double nb = (double)((B + 255) / 256);
+  const double steps_t = ((double)pk->total_keep / pk->T + 32.0) / 32.0;
+  const double steps_g = ((double)g->total_keep / g->T + 32.0) / 32.0;
+  const double waves_t = std::ceil(pk->T * nb / sms), waves_g = std::ceil(g->T / 2 * nb / (sms / 2));
+  const double cyc_t = pk->V <= 64 ? 290.0 : 300.0;
+  return waves_g * steps_g * 200.0 < waves_t * steps_t * cyc_t;
+}
+
+}  // namespace
+
 extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t ldx, int B,
                               uint16_t* Y, int64_t ldy, int out_order, void* stream) {
   using namespace hinm::sm100;
@@ -763,6 +1045,11 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15)) return HINM_ERR_VALUE;
   if (ldx * 2 >= (int64_t)1 << 32) return HINM_ERR_UNSUPPORTED;  // 32-bit row pitch
   if (B == 0 || pk->m == 0) return HINM_OK;
+  if (pk->pair) {  // a union-group pseudo pack given directly: the CTA-pair kernel
+    if (pk->V != 128 || pk->T % 2 || !pk->tile_eofs || pk->rows < 1 || pk->rows > pk->m) return HINM_ERR_VALUE;
+    const int a32 = (ldy % 16) == 0 && ((uintptr_t)Y & 31) == 0;
+    return spmm_pair(pk, X, ldx, B, Y, ldy, out_order, a32, (cudaStream_t)stream);
+  }
   Params prm;
   prm.tile_kofs = pk->tile_kofs;
   prm.tile_eofs = pk->tile_eofs;
@@ -776,6 +1063,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   prm.T = pk->T;
   prm.V = pk->V;
   prm.out_order = out_order;
+  prm.rows = pk->m;
+  prm.tdiv = pk->T;
   // Tuning knobs (environment; every value is validated, an unknown one is an error rather than a
   // silent default).  Defaults are the B200 measurements (scripts/spmm_grid.sh): 8 gather warps (16
   // are no faster: the fill rate under a running MMA is the cap); V <= 64 -> 128-row X stages;
@@ -844,6 +1133,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int variant = kn.variant;
   const int dev = current_device();
   const int sms = sm_count(dev);
+  if (variant == 0 && !kn.xblk && choose_group(pk, B, sms))
+    return spmm_pair(pk->group, X, ldx, B, Y, ldy, out_order, prm.y_align32, (cudaStream_t)stream);
   // 128-token units only when 256-token units would leave more than half the SMs idle (e.g. the
   // down projection at 256 tokens per GPU under 8-way token sharding: 64 units -> 128 units,
   // 0.030 -> 0.024 ms); with more units the 256-token kernel wins

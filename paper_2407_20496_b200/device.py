@@ -69,6 +69,9 @@ class DevicePack:
     a_meta: object = None     # int32 [meta words]
     kpad_cap: int = 0
     meta_cap: int = 0
+    group: "DevicePack | None" = None  # union-group image (build_group_image), used when faster
+    pair: int = 0                      # this is a union-group pseudo pack (256-row groups)
+    rows: int = 0                      # pseudo pack: output rows of the original matrix
 
     @property
     def T(self) -> int:
@@ -101,6 +104,9 @@ class DevicePack:
         s.kpad_cap, s.meta_words_cap = self.kpad_cap, self.meta_cap
         s.tile_kofs, s.tile_eofs = _ptr(self.tile_kofs), _ptr(self.tile_eofs)
         s.gidx, s.a_vals, s.a_meta = _ptr(self.gidx), _ptr(self.a_vals), _ptr(self.a_meta)
+        s.pair, s.rows = self.pair, self.rows
+        if self.group is not None:
+            s.group = ctypes.pointer(self.group.struct())
         object.__setattr__(self, "_struct_cache", s)
         return s
 
@@ -166,7 +172,8 @@ class DevicePack:
             t = getattr(self, name)
             fields[name] = None if t is None else t.to(device, non_blocking=True)
         return DevicePack(self.m, self.n, self.V, self.N, self.M, self.total_keep, self.config,
-                          kpad_cap=self.kpad_cap, meta_cap=self.meta_cap, **fields)
+                          kpad_cap=self.kpad_cap, meta_cap=self.meta_cap, pair=self.pair, rows=self.rows,
+                          group=None if self.group is None else self.group.replicate(device), **fields)
 
 
 def _alloc_operand_image(pack: DevicePack) -> None:
@@ -238,7 +245,7 @@ def _carve(dev, parts):
 
 
 def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None,
-             saliency=None):
+             saliency=None, groups: bool | None = None):
     """Fused GPU compressor (north-star subsystem 1): bf16 W (m x n, CUDA) + sigma -> DevicePack.
 
     ``sigma_o``: permutation of the m output channels; ``sigma_i``: optional per-tile gather
@@ -246,6 +253,8 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
     ascending survivors.  ``saliency``: optional external scores (m x n; numpy / SaliencyMatrix /
     CUDA tensor, fp64 or fp32 -- the reference's ``encode --saliency`` path, cli.py:63-69,189-190);
     default |W|.  Bit-exact with the reference's vector_prune -> nm_prune -> encode.
+    ``groups``: also build the union-group image (:func:`build_group_image`); default: when the
+    operand image is built, V is 32 or 64 and m >= 256.
     """
     torch = _torch()
     _require_cuda(weights, "weights")
@@ -320,6 +329,10 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
                                         ws.data_ptr(), ws_bytes.value, stream)
     _lib.check(status, "compress")
     pack.vector_mask = vmask.view(vcfg.num_tiles, n)
+    if groups is None:
+        groups = build_operand_image and group_supported(pack) and m >= 256
+    if groups:
+        build_group_image(pack)
     return pack
 
 
@@ -338,12 +351,58 @@ def build_operand_image(pack: DevicePack) -> DevicePack:
     return pack
 
 
-def spmm(pack: DevicePack, X, out=None, order: str = "sigma"):
+def group_supported(pack: DevicePack) -> bool:
+    """The union-group image applies to 2:4 packs with V in (32, 64) (256 // V tiles per group)."""
+    return pack.N == 2 and pack.M == 4 and pack.V in (32, 64) and not pack.pair and pack.n <= 32767
+
+
+def build_group_image(pack: DevicePack) -> DevicePack:
+    """Build (or rebuild) the union-group image of ``pack`` (hinm_group_plan + hinm_group_build):
+    256 // V consecutive tiles share one gather list -- the union of their kept vectors, chunked so
+    that every row keeps at most two nonzeros per 4 slots -- and run as one 2:4 matrix of 256 rows on
+    the CTA-pair kernel.  Attached as ``pack.group``; :func:`spmm` uses it when it is the faster image
+    for the call.  Returns the pseudo pack (V = 128 tiles, ``pair`` = 1, ``rows`` = m)."""
+    torch = _torch()
+    if not group_supported(pack):
+        raise ValueError(f"union-group image needs 2:4 and V in (32, 64); got V={pack.V}, {pack.N}:{pack.M}")
+    lib = _lib.load()
+    dev = pack.device
+    st = pack.struct()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.hinm_group_workspace(ctypes.byref(st), ctypes.byref(nbytes)), "group_workspace")
+    U = -(-pack.m // 256)
+    nch = np.zeros(U, dtype=np.int32)
+    with torch.cuda.device(dev):
+        stream = _stream_handle(dev)
+        ws = _workspace(dev, stream, nbytes.value)
+        _lib.check(lib.hinm_group_plan(ctypes.byref(st), ws.data_ptr(), nbytes.value, nch.ctypes.data, stream),
+                   "group_plan")
+        K2 = 8 * int(nch.astype(np.int64).sum())
+        gm, L2 = 256 * U, 128 * K2 // 4 * 2
+        kc, mc, ac = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(lib.hinm_pack_capacity(gm, pack.n, 128, K2, ctypes.byref(kc), ctypes.byref(mc),
+                                          ctypes.byref(ac)), "pack_capacity")
+        a = _carve(dev, [("tile_ptr", torch.int32, 2 * U + 1), ("vec_idx", torch.int32, K2),
+                         ("nm_pos", torch.uint8, L2), ("kept", torch.bfloat16, L2),
+                         ("tile_kofs", torch.int32, 2 * U + 1), ("tile_eofs", torch.int32, 2 * U + 1),
+                         ("gidx", torch.int32, kc.value), ("a_vals", torch.bfloat16, ac.value),
+                         ("a_meta", torch.int32, mc.value)])
+        g = DevicePack(gm, pack.n, 128, 2, 4, K2, pack.config, sigma_o=pack.sigma_o, kpad_cap=kc.value,
+                       meta_cap=mc.value, pair=1, rows=pack.m, **a)
+        gst = g.struct()
+        _lib.check(lib.hinm_group_build(ctypes.byref(st), ws.data_ptr(), nbytes.value, ctypes.byref(gst), stream),
+                   "group_build")
+    pack.group = g
+    return g
+
+
+def spmm(pack: DevicePack, X, out=None, order: str = "sigma", image: str = "auto"):
     """tcgen05 HiNM SpMM: Y (m x B, bf16) = W_hinm @ X (n x B, bf16, channel-major).
 
     ``order='sigma'`` returns rows in sigma_o order (== hinm.hinm_spmm); ``'original'`` fuses
     restore_row_order into the epilogue store.  ``out`` (optional) must be an (m x B) bf16 CUDA
-    tensor with contiguous rows on X's device.
+    tensor with contiguous rows on X's device.  ``image``: ``'auto'`` (the library picks the per-tile
+    or the union-group image, whichever is faster for B tokens), ``'tiles'`` or ``'groups'``.
     """
     torch = _torch()
     _require_cuda(X, "inputs")
@@ -365,7 +424,22 @@ def spmm(pack: DevicePack, X, out=None, order: str = "sigma"):
         raise ValueError(f"out must be a ({pack.m}, {B}) bfloat16 tensor on {X.device} with "
                          "contiguous rows")
     ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
-    st = pack.struct()
+    if image == "auto":
+        st = pack.struct()
+    elif image == "groups":
+        if pack.group is None:
+            raise ValueError("pack has no union-group image (build_group_image)")
+        st = pack.group.struct()
+    elif image == "tiles":
+        st = pack.__dict__.get("_tiles_struct")
+        base = pack.struct()
+        if st is None or st._base is not base:
+            st = _lib.PackStruct.from_buffer_copy(base)
+            st.group = None
+            st._base = base
+            object.__setattr__(pack, "_tiles_struct", st)
+    else:
+        raise ValueError(f"image must be 'auto', 'tiles' or 'groups', got {image!r}")
     lib = _lib.load()
     dev = X.device.index
     if dev != torch.cuda.current_device():

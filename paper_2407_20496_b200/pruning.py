@@ -218,7 +218,7 @@ class HiNMEncoding:
 def pack_from_encoding(enc: HiNMEncoding, device):
     """Upload a host HiNMEncoding and build its tcgen05 operand image on the GPU."""
     torch = _torch()
-    from .device import DevicePack, build_operand_image, spmm_supported
+    from .device import DevicePack, build_group_image, build_operand_image, group_supported, spmm_supported
 
     cfg = enc.config
     V, N, M = cfg.vector_size, cfg.nm_keep, cfg.nm_group
@@ -248,6 +248,8 @@ def pack_from_encoding(enc: HiNMEncoding, device):
         kept=tt(kv).to(torch.bfloat16))
     if spmm_supported(V, N, M):
         build_operand_image(pack)
+        if group_supported(pack) and m >= 256:
+            build_group_image(pack)
     return pack
 
 

@@ -52,6 +52,8 @@ def broadcast_pack(pack, src: int = 0, group=None, device=None):
             "shapes": {k: (None if getattr(pack, k) is None else
                            (tuple(getattr(pack, k).shape), str(getattr(pack, k).dtype)))
                        for k in _PACK_TENSORS},
+            "pair": (pack.pair, pack.rows),
+            "group": pack.group is not None,
         }]
     dist.broadcast_object_list(meta, src=src, group=group)
     meta = meta[0]
@@ -69,10 +71,14 @@ def broadcast_pack(pack, src: int = 0, group=None, device=None):
             t = torch.empty(shape, dtype=dtype, device=device)
         dist.broadcast(t, src=src, group=group)
         tensors[k] = t
+    # the union-group image (if any) travels with its pack
+    group = broadcast_pack(pack.group if rank == src else None, src, group, device) if meta["group"] else None
     if rank == src:
         return pack
     m, n, V, N, M, K, kc, mc = meta["scalars"]
-    return DevicePack(m, n, V, N, M, K, meta["config"], kpad_cap=kc, meta_cap=mc, **tensors)
+    pair, rows = meta["pair"]
+    return DevicePack(m, n, V, N, M, K, meta["config"], kpad_cap=kc, meta_cap=mc, pair=pair, rows=rows,
+                      group=group, **tensors)
 
 
 def gather_tokens(y_local, tokens: int, group=None, align: int = 8):
