@@ -270,29 +270,42 @@ def run_llama(args):
     cfg = H.HiNMConfig(args.v, NM_N, NM_M, SV)
 
     # weights: rank 0 compresses, NCCL replicates the packs (outside the timed region)
-    packs, dense, sos, comp = {}, {}, {}, {}
+    packs, dense, sos, comp, group_ms = {}, {}, {}, {}, {}
     for i, (name, m, n) in enumerate(layer_shapes()):
         g = torch.Generator(device=dev).manual_seed(1000 + i)
         dense[name] = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
         sos[name] = torch.randperm(m, generator=torch.Generator().manual_seed(2000 + i)).numpy()
     if d.rank == 0:
-        # compressor timing: a warm-up pass over the three layers (allocator, pinned staging, cub,
-        # attributes), then the three layers back to back -- host wall and stream time (CUDA events)
-        # per layer, and the whole pass (how a model's layers are compressed)
-        for name in names_of():
-            H.compress(dense[name], cfg, sos[name])
+        # compressor timing (the reference view + per-tile tcgen05 image, hinm_compress_bf16): two
+        # warm-up passes that keep their packs alive (allocator pool, pinned staging, cub,
+        # attributes -- a measured pass must not pay a cudaMalloc), then the three layers back to
+        # back: host wall and stream time (CUDA events) per layer; and the GPU time of one
+        # compression with the host out of the loop (captured once in a CUDA graph, L2 flushed)
+        for _ in range(2):
+            for name in names_of():
+                packs[name] = H.compress(dense[name], cfg, sos[name], groups=False)
         torch.cuda.synchronize()
         ev = _events(torch, 4)
         t_wall = []
         ev[0].record()
         for j, name in enumerate(names_of()):
             t0 = time.perf_counter()
-            packs[name] = H.compress(dense[name], cfg, sos[name])
+            packs[name] = H.compress(dense[name], cfg, sos[name], groups=False)
             t_wall.append((time.perf_counter() - t0) * 1e3)
             ev[j + 1].record()
         torch.cuda.synchronize()
+        gpu_ms = compress_gpu_ms(H, torch, dense, cfg, sos)
         for j, name in enumerate(names_of()):
-            comp[name] = (t_wall[j], ev[j].elapsed_time(ev[j + 1]))
+            comp[name] = (t_wall[j], ev[j].elapsed_time(ev[j + 1]), gpu_ms.get(name))
+        # the union-group image (hinm_group_plan + hinm_group_build): a one-time weight transform
+        # next to the compressor, timed on its own (host wall; it synchronizes twice)
+        if args.v in (32, 64):
+            for name in names_of():
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                H.build_group_image(packs[name])
+                torch.cuda.synchronize()
+                group_ms[name] = (time.perf_counter() - t0) * 1e3
     for name in names_of():
         if d.world > 1:
             packs[name] = broadcast_pack(packs.get(name), src=0, device=dev)
@@ -338,6 +351,11 @@ def run_llama(args):
     pct = lambda q: step_ms[min(len(step_ms) - 1, int(q * (len(step_ms) - 1) + 0.5))]  # noqa: E731
     launches = 3 * args.steps                            # hinm_spmm_bf16 launches one kernel each
     assert lib.hinm_last_launch_count() == 1
+    # which image the library picked per layer (per-tile or union-group), from one more call each
+    per_kernel_image = {}
+    for nm, src in (("gate", X), ("up", X), ("down", y["up"])):
+        H.spmm(packs[nm], src, out=y[nm], order="original")
+        per_kernel_image[nm] = "groups" if lib.hinm_last_image() == 1 else "tiles"
     ms_step = ms_total / args.steps
     value = eff_flops(global_tokens) / (ms_step * 1e-3) / 1e12
 
@@ -400,7 +418,7 @@ def run_llama(args):
     if d.rank == 0:
         result = llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value,
                             ms_cold, cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e,
-                            ms_link, xh, yh, chunk, launches)
+                            ms_link, xh, yh, chunk, launches, group_ms, per_kernel_image)
     # secondary rows (rank 0, N=1 only): the same step at V=128
     if d.world == 1 and not args.no_extras and args.v == 64:
         result["v128"] = v128_row(H, torch, dev, X, y, args, cublas, global_tokens)
@@ -411,9 +429,54 @@ def run_llama(args):
     d.close()
 
 
+def compress_gpu_ms(H, torch, dense, cfg, sos, reps=5):
+    """GPU time of one compression per layer with the host out of the loop: the call captured once
+    in a CUDA graph (its allocations come from the graph pool), replayed after an L2 flush."""
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dense["up"].device)
+    for name in names_of():
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.stream(s):
+                H.compress(dense[name], cfg, sos[name], groups=False)  # warm (workspace, attributes)
+                with torch.cuda.graph(g, stream=s):
+                    H.compress(dense[name], cfg, sos[name], groups=False)
+        except Exception:  # pragma: no cover - capture unsupported: report stream time only
+            continue
+        torch.cuda.current_stream().wait_stream(s)
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = _events(torch, 2)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[name] = statistics.median(ts)
+    return out
+
+
+def pair_floor(pack, tokens, sms=148):
+    """Tensor-pipe floor of a union-group launch: every CTA pair runs one M=256 N=256 K=32 sparse
+    MMA per 128 cycles (scripts/probe_2sm.cu); units = groups x 256-token blocks over sms/2 pairs."""
+    g = pack.group
+    if g is None:
+        return None
+    U = g.T // 2
+    ku = g.total_keep // g.T
+    kp = -(-ku // 64) * 64
+    units = U * -(-tokens // 256)
+    waves = -(-units // (sms // 2))
+    return {"groups": U, "K_union": ku, "K_tile": pack.total_keep // pack.T, "units": units,
+            "mma_cycles": waves * (kp // 32) * 128}
+
+
 def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value, ms_cold,
                cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e, ms_link, xh, yh, chunk,
-               launches):
+               launches, group_ms, per_kernel_image):
     pk, kind = peaks()
     p_sparse = 2.0 * pk["bf16_tflops"]
     f_sp = sparse_flops(tokens)
@@ -421,11 +484,18 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
     # dominant kernel: the gate / up projection (11008 x 4096), per launch
     f_up = 2.0 * M_FFN * int(N_FFN * (1 - SV)) * tokens
     ach_up = f_up / (per_kernel["up"] * 1e-3) / 1e12
-    # the gather: every kept K-row of a tile is streamed L2 -> SMEM once per 256-token block
-    # (2 * T * k_bar * tokens bytes) plus the compressed A / metadata image per unit
-    gathered = sum(2.0 * (m // args.v) * int(n * (1 - SV)) * tokens for _, m, n in layer_shapes())
-    a_image = sum((m // args.v) * int(n * (1 - SV)) * args.v * 1.125 * -(-tokens // 256)
-                  for _, m, n in layer_shapes())
+    # the gather: every kept K-row of an image tile (per-tile image: a V-row tile's k_bar rows;
+    # union-group image: a 256-row group's K_u rows) is streamed L2 -> SMEM once per 256-token
+    # block, plus the compressed A / metadata image per unit
+    gathered = a_image = 0.0
+    for name, m, n in layer_shapes():
+        pf = pair_floor(packs[name], tokens)
+        if pf is not None and per_kernel_image.get(name) == "groups":
+            gathered += 2.0 * pf["groups"] * pf["K_union"] * tokens
+            a_image += pf["groups"] * pf["K_union"] * 256 * 1.125 * -(-tokens // 256)
+        else:
+            gathered += 2.0 * (m // args.v) * int(n * (1 - SV)) * tokens
+            a_image += (m // args.v) * int(n * (1 - SV)) * args.v * 1.125 * -(-tokens // 256)
     l2_bclk = None
     l2_tbs = (gathered + a_image) / (sum(per_kernel.values()) * 1e-3) / 1e12
     ceiling = None if args.no_extras else gather_ceiling()
@@ -452,6 +522,20 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
         comp_bytes += 2 * m * n + m * kbar + m * kbar // 8 + 4 * (m // args.v) * kbar + 4 * m
     comp_ms = sum(c[0] for c in comp.values())
     comp_gpu = sum(c[1] for c in comp.values())
+    comp_graph = sum(c[2] for c in comp.values() if c[2] is not None) if all(c[2] for c in comp.values()) else None
+    pf_up = pair_floor(packs["up"], tokens)
+    sm_ghz = (clk.summary().get("sm_mhz") or 1965.0) / 1e3
+    pair_info = None
+    if pf_up is not None and per_kernel_image.get("up") == "groups":
+        floor_ms = pf_up["mma_cycles"] / (sm_ghz * 1e6)
+        pair_info = {"image": "union-group (256-row groups, CTA-pair tcgen05.mma.sp.cta_group::2 M=256 N=256)",
+                     "K_tile": pf_up["K_tile"], "K_union": pf_up["K_union"],
+                     "useful_fraction_of_mma_work": round(pf_up["K_tile"] / pf_up["K_union"], 4),
+                     "mma_floor_ms_at_sampled_clock": round(floor_ms, 4),
+                     "frac_of_mma_floor": round(floor_ms / per_kernel["up"], 4),
+                     "note": "floor = waves x K-steps x 128 cycles per CTA-pair MMA (scripts/probe_2sm.cu); the "
+                             "kernel's effective SM clock under load is lower than the NVML sample "
+                             "(profiles/r03_pair.txt)"}
     strong = not args.weak
     return {
         "metric": METRIC,
@@ -485,6 +569,7 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                               "clocks": clk_cublas.summary(),
                               "protocol": "same W/K step protocol as value, after a 1 s pause"},
         "per_spmm_ms": {k: round(v, 4) for k, v in per_kernel.items()},
+        "per_spmm_image": per_kernel_image,
         "roofline": {"bound": "tensor", "achieved": round(ach_up, 1), "peak": round(p_sparse, 1),
                      "unit": "TFLOP/s", "frac": round(ach_up / p_sparse, 4), "traffic": traffic,
                      "kernel": "k_hinm_spmm, up projection 11008x4096 (the dominant launch)",
@@ -495,17 +580,25 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                      "traffic_note": (tr or {}).get("note"),
                      # the V=64 tile runs on the M=64 sparse instruction: 144 cycles per
                      # 64x256x32 MMA = 1964 TF/s on 148 SMs at 1.965 GHz (scripts/mma_rate.cu)
-                     "instruction_ceiling": 1964.4,
-                     "frac_of_instruction_ceiling": round(ach_up / 1964.4, 4),
+                     "instruction_ceiling": None if pair_info else 1964.4,
+                     "frac_of_instruction_ceiling": None if pair_info else round(ach_up / 1964.4, 4),
+                     "pair_kernel": pair_info,
                      "binding": binding},
         "compressor": {"ms": {k: round(v[0], 3) for k, v in comp.items()},
                        "stream_ms": {k: round(v[1], 3) for k, v in comp.items()},
+                       "gpu_ms": {k: (None if v[2] is None else round(v[2], 4)) for k, v in comp.items()},
                        "algorithmic_bytes": comp_bytes,
                        "gbs": round(comp_bytes / (comp_ms * 1e-3) / 1e9, 1),
                        "gbs_stream": round(comp_bytes / (comp_gpu * 1e-3) / 1e9, 1),
                        "hbm_frac_stream": round(comp_bytes / (comp_gpu * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
-                       "note": "the three layers compressed back to back after a warm-up pass: ms = host "
-                               "wall per call, stream_ms = CUDA events between consecutive calls; rank 0"},
+                       "hbm_frac_gpu": None if not comp_graph else
+                       round(comp_bytes / (comp_graph * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                       "union_group_image_ms": {k: round(v, 2) for k, v in group_ms.items()},
+                       "note": "hinm_compress_bf16 (reference view + per-tile image), three layers back to back "
+                               "after two warm-up passes: ms = host wall per call, stream_ms = CUDA events "
+                               "between consecutive calls, gpu_ms = one call captured in a CUDA graph and "
+                               "replayed after an L2 flush; union_group_image_ms = hinm_group_plan + "
+                               "hinm_group_build (a one-time weight transform, host wall); rank 0"},
         "e2e": {"value": round(eff_flops(global_tokens) / (ms_e2e * 1e-3) / 1e12, 2),
                 "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(yh.numel() * 2),

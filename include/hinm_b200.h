@@ -238,6 +238,8 @@ int hinm_group_build(const hinm_pack_t* pack, void* workspace, size_t workspace_
 
 /* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
 int hinm_last_launch_count(void);
+/* Image the most recent hinm_spmm_bf16 call on this thread ran: 0 per-tile, 1 union-group. */
+int hinm_last_image(void);
 
 /*
  * Gyro-permutation search kernels (the search driver is

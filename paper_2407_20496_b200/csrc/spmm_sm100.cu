@@ -229,6 +229,7 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
 // clocks right after the start-up cluster barrier (offset calibration).
 #ifdef HINM_TRACE
 __device__ unsigned long long g_trace[11][1024];
+__device__ unsigned long long g_utrace[160][72];  // per CTA: globaltimer at start, then per unit (MMA warp)
 #define TRACE(ev, i)                                                                     \
   do {                                                                                   \
     if (blockIdx.x < 2 && (i) < 1024) g_trace[ev][i] = (unsigned long long)clock64();    \
@@ -368,7 +369,11 @@ __host__ __device__ constexpr int gather_warp0(int GW) { return GW == 8 ? 10 : 1
 // its sub-partition and, through the barrier, the whole stage: the leader's stage fill took ~700
 // cycles longer than the peer's, also with the gather itself disabled (scripts/pair_trace.py).
 // Warps 12 and 16 stay idle.
+#ifdef HINM_SPREAD_ALL
+__host__ __device__ constexpr bool gather_spread(int GW, bool) { return GW == 8; }
+#else
 __host__ __device__ constexpr bool gather_spread(int GW, bool pair) { return pair && GW == 8; }
+#endif
 __host__ __device__ constexpr int kernel_warps(int GW, bool pair) {
   return gather_spread(GW, pair) ? 20 : gather_warp0(GW) + GW;
 }
@@ -505,6 +510,10 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
   __syncthreads();
   if (PAIR) cluster_sync();  // barrier inits visible to the peer before any remote arrive
   if (threadIdx.x == 0) TRACE(10, crank);
+#ifdef HINM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_utrace[blockIdx.x][0] = globaltimer();
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_trace[8][blockIdx.x] = clock64();
+#endif
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const int T = p.T;
@@ -754,6 +763,10 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
       }
       if (elect_one()) tc_commit_x<PAIR>(bar_acc_full + 8 * acc);
       __syncwarp();
+#ifdef HINM_TRACE
+      if (lane == 0 && blockIdx.x < 160 && acc_uses < 71) g_utrace[blockIdx.x][acc_uses] = globaltimer();
+      if (lane == 0 && blockIdx.x < 160 && acc_uses < 71) g_trace[9][blockIdx.x * 4 + (acc_uses & 3)] = clock64();
+#endif
     }
   } else if (warp < EPI_WARPS) {
     // ============================================================ epilogue (warps 0-7)
@@ -908,6 +921,7 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
 namespace {
 
 thread_local int g_last_launches = 0;
+thread_local int g_last_image = 0;  // 0: per-tile image, 1: union-group image (CTA pair)
 
 // Per-device SM count and per-(kernel, device) shared-memory opt-in, cached: the launch path is
 // on the critical path of short SpMMs (host time per call, scripts/host_overhead.py).
@@ -935,12 +949,19 @@ cudaError_t ensure_smem(const void* fn, int /*dev*/, int bytes) { return hinm::s
 }  // namespace
 
 extern "C" int hinm_last_launch_count(void) { return g_last_launches; }
+extern "C" int hinm_last_image(void) { return g_last_image; }
 
 #ifdef HINM_TRACE
 // experiments: copy the pair-0 event trace (11 x 1024 clock64 values) to host memory
 extern "C" int hinm_exp_trace(unsigned long long* host) {
   HINM_CUDA_TRY(cudaDeviceSynchronize());
   HINM_CUDA_TRY(cudaMemcpyFromSymbol(host, hinm::sm100::g_trace, sizeof(unsigned long long) * 11 * 1024));
+  return HINM_OK;
+}
+extern "C" int hinm_exp_utrace(unsigned long long* host) {
+  HINM_CUDA_TRY(cudaDeviceSynchronize());
+  HINM_CUDA_TRY(cudaMemcpyFromSymbol(host, hinm::sm100::g_utrace, sizeof(unsigned long long) * 160 * 72));
+  HINM_CUDA_TRY(cudaMemset(nullptr, 0, 0));
   return HINM_OK;
 }
 #endif
@@ -1003,6 +1024,7 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
   HINM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, X, ldx, prm));
   HINM_LAUNCH_CHECK();
   g_last_launches = 1;
+  g_last_image = 1;
   return HINM_OK;
 }
 
@@ -1037,6 +1059,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
                               uint16_t* Y, int64_t ldy, int out_order, void* stream) {
   using namespace hinm::sm100;
   g_last_launches = 0;
+  g_last_image = 0;
   if (!pk || !X || !Y) return HINM_ERR_VALUE;
   if (pk->N != 2 || pk->M != 4) return HINM_ERR_UNSUPPORTED;
   if (pk->V != 32 && pk->V != 64 && pk->V != 128) return HINM_ERR_UNSUPPORTED;
@@ -1162,7 +1185,7 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
     HINM_CUDA_TRY(ensure_smem((const void*)kern, dev, (int)L.total));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(32 * (gather_warp0(gw) + gw));
+    cfg.blockDim = dim3(32 * kernel_warps(gw, false));
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

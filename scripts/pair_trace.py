@@ -32,7 +32,15 @@ S = min(S, 1024) - 8
 rng = slice(40, S)
 md = lambda a: float(np.median(a[rng]))
 print(f"stages traced {S}; peer clock offset {off:.0f}")
-print(f"issue interval (L_pfull[i+1]-L_pfull[i])        {float(np.median(np.diff(Lpfull)[40:S])):8.0f}")
+d = np.diff(Lpfull)[40:S]
+print(f"issue interval (L_pfull[i+1]-L_pfull[i])        median {float(np.median(d)):8.0f} mean {float(d.mean()):8.0f} "
+      f"p90 {float(np.percentile(d, 90)):8.0f} p99 {float(np.percentile(d, 99)):8.0f}")
+big = np.nonzero(d > 1500)[0] + 40
+print("stages after gaps > 1500 clk:", big[:40].tolist())
+for i in big[:6]:
+    print(f"  gap at {i}->{i+1}: {d[i-40]:.0f}; L_go {Lgo[i+1]-Lpfull[i]:.0f} L_full {Lfull[i+1]-Lpfull[i]:.0f} "
+          f"L_afull {Lafull[i+1]-Lpfull[i]:.0f} P_full {Pfull[i+1]-Lpfull[i]:.0f} P_afull {Pafull[i+1]-Lpfull[i]:.0f} "
+          f"LA_go {LAgo[i+1]-Lpfull[i]:.0f} PA_go {PAgo[i+1]-Lpfull[i]:.0f}")
 print(f"leader fill latency  (L_full - L_go)             {md(Lfull - Lgo):8.0f}")
 print(f"peer fill latency    (P_full - P_go)             {md(Pfull - Pgo):8.0f}")
 print(f"leader: pfull after full                          {md(Lpfull - Lfull):8.0f}")

@@ -146,12 +146,21 @@ def test_pair_spmm_llama_shapes_sampled():
         np.testing.assert_allclose(Y[:, cols], ref, rtol=RTOL, atol=ATOL)
 
 
-def test_auto_picks_groups_for_long_token_counts():
+def test_auto_picks_images_by_token_count():
+    """The per-call choice: the union-group image at LLaMA scale, the per-tile image where the
+    pairs would idle (a 768-row layer at 256 tokens: 3 groups vs 12 tiles)."""
+    from paper_2407_20496_b200 import _lib
+
+    lib = _lib.load()
     _, _, _, pack = _pack(11008, 4096, 64, 0.5, seed=31)
     X = torch.zeros(4096, 16384, dtype=torch.bfloat16, device="cuda")
     H.spmm(pack, X)
-    lib = __import__("paper_2407_20496_b200._lib", fromlist=["load"]).load()
-    assert lib.hinm_last_launch_count() == 1
+    assert lib.hinm_last_launch_count() == 1 and lib.hinm_last_image() == 1
+    H.spmm(pack, X, image="tiles")
+    assert lib.hinm_last_image() == 0
+    _, _, _, small = _pack(768, 768, 64, 0.5, seed=32)
+    H.spmm(small, torch.zeros(768, 256, dtype=torch.bfloat16, device="cuda"))
+    assert lib.hinm_last_image() == 0
 
 
 def test_replicate_keeps_group():
