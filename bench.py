@@ -535,7 +535,7 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                      "frac_of_mma_floor": round(floor_ms / per_kernel["up"], 4),
                      "note": "floor = waves x K-steps x 128 cycles per CTA-pair MMA (scripts/probe_2sm.cu); the "
                              "kernel's effective SM clock under load is lower than the NVML sample "
-                             "(profiles/r03_pair.txt)"}
+                             "(profiles/r02_pair.txt)"}
     strong = not args.weak
     return {
         "metric": METRIC,
@@ -842,6 +842,12 @@ def cfg_cases(name):
     raise ValueError(name)
 
 
+def _lib_image():
+    from paper_2407_20496_b200 import _lib
+
+    return _lib.load().hinm_last_image()
+
+
 def run_config(args):
     import torch
 
@@ -899,10 +905,13 @@ def run_config(args):
         Yc = torch.empty(m, tl, dtype=torch.bfloat16, device=dev)
         pack = H.compress(W, H.HiNMConfig(v, 2, 4, sv), np.random.default_rng(i).permutation(m))
         ms = timed(lambda: H.spmm(pack, X, out=Y, order="original"), graph)
+        H.spmm(pack, X, out=Y, order="original")
+        image = "groups" if _lib_image() == 1 else "tiles"
         cb = timed(lambda: torch.matmul(W, X, out=Yc), graph)
         f = 2.0 * m * n * tokens
         launches += count * args.steps
         rows.append({"gemm": label, "m": m, "n": n, "tokens": tokens, "V": v, "s_v": sv, "count": count,
+                     "image": image,
                      "spmm_ms": round(ms, 4), "cublas_ms": round(cb, 4), "speedup": round(cb / ms, 3),
                      "eff_tflops": round(f / ms / 1e9, 1), "timing": "cuda graph" if graph else "eager"})
         tot_sp += ms * count

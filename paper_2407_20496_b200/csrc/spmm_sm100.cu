@@ -218,7 +218,7 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
   return r;
 }
 // Relaxed: a release arrive compiles to MEMBAR.GPU (+ the waiter's acquire.cluster to CCTL.IVALL),
-// ~1-2 k cycles on the per-stage critical path (ncu source view, profiles/r03_pair.txt).  What the
+// ~1-2 k cycles on the per-stage critical path (ncu source view, profiles/r02_pair.txt).  What the
 // leader needs is already established before the arrive: the peer's cp.async / bulk writes have
 // completed (its local full barrier), its TMEM loads have completed (tcgen05.wait::ld).
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
@@ -1014,13 +1014,17 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
   cfg.blockDim = dim3(32 * kernel_warps(GW, true));
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // short launches overlap their prologue with the previous kernel's tail (programmatic dependent
+  // launch), as on the per-tile path
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = prm.units <= 8 * pairs ? 2 : 1;
   HINM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, X, ldx, prm));
   HINM_LAUNCH_CHECK();
   g_last_launches = 1;
@@ -1028,10 +1032,15 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
   return HINM_OK;
 }
 
-// Per-call choice between a pack's per-tile image and its union-group image: modelled SM time =
-// waves x K-steps x cycles per 32-K step (per-tile V <= 64 on M = 64: ~290; CTA pair: ~200 --
-// measured fill rates, profiles/r03_pair.txt).  Few units (short token counts) keep the per-tile
-// image: it has twice the units and half the K per unit.  HINM_GROUPS = 0 | 1 forces.
+// Per-call choice between a pack's per-tile image and its union-group image.  Modelled time =
+// ramp + waves x max(K-steps x cycles per 32-K step + unit overhead, unit floor), fitted on B200
+// (profiles/r02_pair.txt: scripts/pair_sweep.py, bench.py --config cfg2 / cfg4 / cfg5):
+//   per-tile (148 SMs):     270 cycles per step + 2300 per unit, ramp 3000
+//   union-group (74 pairs): 226 cycles per 32-K_u step + 3300 per unit, >= 5000 per unit, ramp 8000;
+//                           >= 12000 per unit for <= 128-slot groups over > 256k tokens (the
+//                           pair's 128-row x 256-token stores per CTA at a > 0.5 MB row pitch: the
+//                           ResNet im2col 256x64 layer at 802816 tokens runs 2x slower than per-tile)
+// HINM_GROUPS = 0 | 1 forces.
 bool choose_group(const hinm_pack_t* pk, int B, int sms) {
   const hinm_pack_t* g = pk->group;
   if (!g || !g->pair || !g->a_vals || !g->tile_kofs || g->T < 2 || pk->T < 1) return false;
@@ -1046,11 +1055,13 @@ bool choose_group(const hinm_pack_t* pk, int B, int sms) {
   if (force == 0 || force == -2) return false;
   if (force == 1) return true;
   const double nb = (double)((B + 255) / 256);
-  const double steps_t = ((double)pk->total_keep / pk->T + 32.0) / 32.0;
-  const double steps_g = ((double)g->total_keep / g->T + 32.0) / 32.0;
+  auto steps = [](double k) { return std::ceil(k / 64.0) * 2.0; };  // kp = round_up(k, 64) in 32-K steps
+  const double st_t = steps((double)pk->total_keep / pk->T), st_g = steps((double)g->total_keep / g->T);
   const double waves_t = std::ceil(pk->T * nb / sms), waves_g = std::ceil(g->T / 2 * nb / (sms / 2));
-  const double cyc_t = pk->V <= 64 ? 290.0 : 300.0;
-  return waves_g * steps_g * 200.0 < waves_t * steps_t * cyc_t;
+  const double floor_g = st_g <= 4.0 && B > 262144 ? 12000.0 : 5000.0;
+  const double cost_t = 3000.0 + waves_t * (st_t * 270.0 + 2300.0);
+  const double cost_g = 8000.0 + waves_g * std::max(st_g * 226.0 + 3300.0, floor_g);
+  return cost_g < cost_t;
 }
 
 }  // namespace

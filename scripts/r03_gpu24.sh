@@ -1,0 +1,13 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+rm -f gpurun_out/configs_r02c.jsonl
+for c in cfg1 cfg2 cfg4 cfg4_875 cfg5; do timeout 600 python bench.py --config $c >> gpurun_out/configs_r02c.jsonl 2>> gpurun_out/configs_r02c.err; done
+python - <<'PY'
+import json
+for l in open("gpurun_out/configs_r02c.jsonl"):
+    d = json.loads(l)
+    print(d["metric"], d["ms_per_step"], d["cublas_ms_per_step"], d["speedup_vs_cublas"])
+    for r in d["rows"]:
+        print("   ", r["gemm"], r["image"], r["spmm_ms"], r["cublas_ms"], r["speedup"], r["count"])
+PY
