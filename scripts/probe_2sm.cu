@@ -67,6 +67,8 @@ constexpr int E_BYTES = 128 * 16;         // 128 lanes x 4 words
 constexpr int E_COL = 256;
 
 // ------------------------------------------------------------------------------ part 1
+constexpr int A_COL = 320;  // TMEM columns of the A copies (TS variant): 4 MMA steps x 8 columns
+template <bool ATMEM>
 __global__ void __cluster_dims__(2, 1, 1) probe(const uint8_t* __restrict__ a_img, const uint8_t* __restrict__ b_img,
                                                 const uint8_t* __restrict__ e_img, float* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -107,11 +109,20 @@ __global__ void __cluster_dims__(2, 1, 1) probe(const uint8_t* __restrict__ a_im
         const uint64_t ad = ad0 + (uint64_t)((i * 32 * 128) >> 4);
         const uint64_t bd = bd0 + (uint64_t)((i * 4096) >> 4);
         const uint32_t ecol = tmem + E_COL + (i >> 1) * 2;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t}\n" ::"r"(tmem),
-            "l"(ad), "l"(bd), "r"(idesc | (uint32_t)(i & 1)), "r"(i), "r"(ecol)
-            : "memory");
+        if (ATMEM) {  // A of this step: smem image -> TMEM (128 lanes x 256 bits), then the TS MMA
+          asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(tmem + A_COL + 8 * i), "l"(ad) : "memory");
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [%1], %2, [%5], %3, p;\n\t}\n" ::"r"(tmem),
+              "r"(tmem + A_COL + 8 * i), "l"(bd), "r"(idesc | (uint32_t)(i & 1)), "r"(i), "r"(ecol)
+              : "memory");
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t}\n" ::"r"(tmem),
+              "l"(ad), "l"(bd), "r"(idesc | (uint32_t)(i & 1)), "r"(i), "r"(ecol)
+              : "memory");
+        }
       }
       asm volatile(
           "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -372,8 +383,11 @@ int main() {
   cudaMemcpy(de, eimg.data(), 2 * E_BYTES, cudaMemcpyHostToDevice);
   cudaMemset(dout, 0, 2 * 128 * 256 * 4);
   const int psmem = A_BYTES + B_BYTES + E_BYTES + 1024;
-  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
-  probe<<<2, 128, psmem>>>(da, db, de, dout);
+  for (int variant = 0; variant < 2; ++variant) {
+  auto pk = variant ? probe<true> : probe<false>;
+  cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+  cudaMemset(dout, 0, 2 * 128 * 256 * 4);
+  pk<<<2, 128, psmem>>>(da, db, de, dout);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("probe error %s\n", cudaGetErrorString(e));
@@ -395,8 +409,9 @@ int main() {
         }
         zero += got == 0.f;
       }
-  printf("probe 2sm M=256 N=256 sparse (B split by N, metadata via tcgen05.cp.cta_group::2): %ld / %d mismatches (%ld zeros)\n",
-         bad, 2 * 128 * 256, zero);
+  printf("probe 2sm M=256 N=256 sparse, A %s (B split by N, metadata via tcgen05.cp.cta_group::2): %ld / %d mismatches (%ld zeros)\n",
+         variant ? "in TMEM (tcgen05.cp 128x256b of the smem image, TS MMA)" : "in smem (SS MMA)", bad, 2 * 128 * 256, zero);
+  }
   // ---- part 2
   const int region_rows = 8192;
   uint4* src;
