@@ -541,6 +541,7 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
       const uint32_t* esrc0 = p.a_meta + (int64_t)cur.e0 * V * 4;
       for (int s = 0; s < nst; s += KS / BK) {             // one A stage per X stage
         mbar_wait(bar_aempty + 8 * aslot, aphase ^ 1);
+        if (DBG == 8) mbar_wait(bar_afull + 8 * aslot, aphase ^ 1);  // experiment: previous copy landed
         if (lane == 0) TRACE(7 + crank, a_count);
         ++a_count;
         const uint32_t fb = bar_afull + 8 * aslot;
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
       for (int s0 = 0; s0 < kp / BK; s0 += KS / BK) {
         mbar_wait(bar_full + 8 * stage, phase);
         if (lane == 0) TRACE(3, r_count);
-        mbar_wait(bar_afull + 8 * aslot, aphase);
+        if (DBG != 8) mbar_wait(bar_afull + 8 * aslot, aphase);
         if (lane == 0) TRACE(4, r_count);
         ++r_count;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
         const bool two = SUB == 2 && s0 + 1 < nst;
         mbar_wait(bar_full + 8 * stage, phase);
         if (lane == 0) TRACE(0, m_count);
-        mbar_wait(bar_afull + 8 * aslot, aphase);
+        if (DBG != 8) mbar_wait(bar_afull + 8 * aslot, aphase);  // experiment 8: A loads off the critical path
         if (lane == 0) TRACE(1, m_count);
         if (PAIR) mbar_wait(bar_pfull + 8 * stage, phase);  // the peer's stage too (relayed)
         if (lane == 0) TRACE(2, m_count);
@@ -1005,6 +1006,8 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
     if (e[0] == '1') kern = k_hinm_spmm<128, 8, 1, false, 128, true>;
     if (e[0] == '2') kern = k_hinm_spmm<128, 8, 2, false, 128, true>;
     if (e[0] == '3') kern = k_hinm_spmm<128, 8, 3, false, 128, true>;
+    if (e[0] == '4') kern = k_hinm_spmm<128, 8, 4, false, 128, true>;
+    if (e[0] == '8') kern = k_hinm_spmm<128, 8, 8, false, 128, true>;
   }
 #endif
   const SmemLayout L = smem_layout(128, KS, false, 128, true);
