@@ -83,3 +83,41 @@ def test_sass_has_tcgen05_and_tma():
     sass = subprocess.run([cuobjdump, "-sass", _lib_path()], capture_output=True, text=True).stdout
     for mnem in ("UTCHMMA", "UTCCP", "LDTM", "UBLKCP", "LDGSTS", "ENL2.256"):
         assert mnem in sass, mnem
+
+
+def test_group_image_host_queries_without_gpu():
+    """hinm_group_workspace validates the pack and sizes the plan / build workspace on the host;
+    configurations outside the union-group image are rejected before any device work."""
+    from paper_2407_20496_b200 import _lib
+
+    lib = _lib.load(_lib_path())
+    dummy = ctypes.c_int32(0)
+    st = _lib.PackStruct()
+    st.m, st.n, st.V, st.N, st.M, st.T = 11008, 4096, 64, 2, 4, 11008 // 64
+    for f in ("tile_ptr", "vec_idx", "nm_pos", "kept_bf16"):
+        setattr(st, f, ctypes.addressof(dummy))
+    nb = ctypes.c_size_t()
+    assert lib.hinm_group_workspace(ctypes.byref(st), ctypes.byref(nb)) == 0
+    U = -(-11008 // 256)
+    assert nb.value >= st.T * 4096 * 2 + U * 4096 * 32 + U * 4096 * 16
+    st.V = 128  # V = 128 has no union-group image
+    assert lib.hinm_group_workspace(ctypes.byref(st), ctypes.byref(nb)) == 10
+    st.V, st.N = 64, 1  # 1:4 is not 2:4
+    assert lib.hinm_group_workspace(ctypes.byref(st), ctypes.byref(nb)) == 10
+    assert lib.hinm_last_image() == 0
+
+
+def test_sass_has_cta_pair_mma():
+    """The union-group path is compiled to the CTA-pair instruction forms: 2-CTA sparse MMA, the
+    pair's TMEM copies and multicast commits (UTCHMMA.2CTA, UTCBAR.2CTA.MULTICAST)."""
+    import shutil
+    import subprocess
+
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        import pytest
+
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([cuobjdump, "-sass", _lib_path()], capture_output=True, text=True).stdout
+    for mnem in ("UTCHMMA.2CTA", "UTCBAR.2CTA.MULTICAST"):
+        assert mnem in sass, mnem

@@ -60,7 +60,16 @@ def _worker(rank, world, port, results):
                 vec_idx=torch.as_tensor(np.concatenate([t[0] for t in ref["tiles"]]).astype(np.int32)),
                 nm_pos=torch.as_tensor(np.concatenate([t[1].ravel() for t in ref["tiles"]]).astype(np.uint8)),
                 kept=torch.as_tensor(np.concatenate([t[2].ravel() for t in ref["tiles"]]).astype(np.float32)).to(torch.bfloat16))
+        if rank == 0:
+            # a union-group pseudo pack rides along (pair / rows flags and its own tensors)
+            pack.group = DevicePack(256, n, 128, 2, 4, 8, HiNMConfig(V, 2, 4, 0.5), sigma_o=pack.sigma_o,
+                                    tile_ptr=torch.tensor([0, 4, 8], dtype=torch.int32),
+                                    vec_idx=torch.arange(8, dtype=torch.int32),
+                                    nm_pos=torch.zeros(512, dtype=torch.uint8),
+                                    kept=torch.zeros(512, dtype=torch.bfloat16), pair=1, rows=m)
         got = broadcast_pack(pack, src=0, device="cpu")
+        assert got.group is not None and got.group.pair == 1 and got.group.rows == m
+        assert torch.equal(got.group.tile_ptr, torch.tensor([0, 4, 8], dtype=torch.int32))
         tiles = got.to_host_tiles()
         for (a, b, c), (x, y, z) in zip(tiles, ref["tiles"]):
             assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
