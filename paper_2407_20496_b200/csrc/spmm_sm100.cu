@@ -549,10 +549,18 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
           // (DBG 7: on every other token block, i.e. the A image read once per 512 tokens)
           if (elect_one()) mbar_arrive(fb);
         } else if (elect_one()) {
-          const uint32_t a_bytes = V * 64 * min(KS / BK, nst - s);
-          const uint32_t e_bytes = (s & 1) ? 0 : V * 16;   // metadata per 128-K block
+          // (experiment 9: ~58 % of the A bytes -- what a compact A image would move; garbage)
+          const uint32_t a_bytes = DBG == 9 ? (V * 64 * min(KS / BK, nst - s) * 9 / 16) & ~15u
+                                            : V * 64 * min(KS / BK, nst - s);
+          const uint32_t e_bytes = (s & 1) || DBG == 10 ? 0 : V * 16;   // metadata per 128-K block (10: skipped)
           mbar_expect_tx(fb, a_bytes + e_bytes);
-          bulk_g2s_hint(sA + aslot * a_slot, asrc + (int64_t)s * BK * V / 2, a_bytes, fb, pol_a);
+          if (DBG == 11) {  // experiment: the A stage as one copy per 32-K MMA step
+            for (uint32_t o = 0; o < a_bytes; o += 32 * V)
+              bulk_g2s_hint(sA + aslot * a_slot + o, reinterpret_cast<const char*>(asrc + (int64_t)s * BK * V / 2) + o,
+                            32 * V, fb, pol_a);
+          } else {
+            bulk_g2s_hint(sA + aslot * a_slot, asrc + (int64_t)s * BK * V / 2, a_bytes, fb, pol_a);
+          }
           if (e_bytes) {
             const uint32_t* esrc = esrc0 + (int64_t)(s / 2) * V * 4;
             if (M64) {  // 16-lane groups of the stored (M=128 order) image -> lanes 32q + 0..15
@@ -1008,6 +1016,9 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
     if (e[0] == '3') kern = k_hinm_spmm<128, 8, 3, false, 128, true>;
     if (e[0] == '4') kern = k_hinm_spmm<128, 8, 4, false, 128, true>;
     if (e[0] == '8') kern = k_hinm_spmm<128, 8, 8, false, 128, true>;
+    if (e[0] == '9') kern = k_hinm_spmm<128, 8, 9, false, 128, true>;
+    if (!strcmp(e, "10")) kern = k_hinm_spmm<128, 8, 10, false, 128, true>;
+    if (!strcmp(e, "11")) kern = k_hinm_spmm<128, 8, 11, false, 128, true>;
   }
 #endif
   const SmemLayout L = smem_layout(128, KS, false, 128, true);
