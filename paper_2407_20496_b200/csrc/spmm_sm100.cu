@@ -1050,7 +1050,8 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
 // ramp + waves x max(K-steps x cycles per 32-K step + unit overhead, unit floor), fitted on B200
 // (profiles/r02_pair.txt: scripts/pair_sweep.py, bench.py --config cfg2 / cfg4 / cfg5):
 //   per-tile (148 SMs):     270 cycles per step + 2300 per unit, ramp 3000
-//   union-group (74 pairs): 226 cycles per 32-K_u step + 3300 per unit, >= 5000 per unit, ramp 8000;
+//   union-group (74 pairs): 226 cycles per 32-K_u step + 3300 per unit, >= 5000 per unit, ramp 8000
+//                           (5000 for launches short enough for PDL);
 //                           >= 12000 per unit for <= 128-slot groups over > 256k tokens (the
 //                           pair's 128-row x 256-token stores per CTA at a > 0.5 MB row pitch: the
 //                           ResNet im2col 256x64 layer at 802816 tokens runs 2x slower than per-tile)
@@ -1074,7 +1075,9 @@ bool choose_group(const hinm_pack_t* pk, int B, int sms) {
   const double waves_t = std::ceil(pk->T * nb / sms), waves_g = std::ceil(g->T / 2 * nb / (sms / 2));
   const double floor_g = st_g <= 4.0 && B > 262144 ? 12000.0 : 5000.0;
   const double cost_t = 3000.0 + waves_t * (st_t * 270.0 + 2300.0);
-  const double cost_g = 8000.0 + waves_g * std::max(st_g * 226.0 + 3300.0, floor_g);
+  // short pair launches overlap their prologue with the previous kernel (PDL): a smaller ramp
+  const double ramp_g = g->T / 2 * nb <= 8.0 * (sms / 2) ? 5000.0 : 8000.0;
+  const double cost_g = ramp_g + waves_g * std::max(st_g * 226.0 + 3300.0, floor_g);
   return cost_g < cost_t;
 }
 
