@@ -102,6 +102,7 @@ class ClockSampler:
         self.index = index
         self.period = period_s
         self.samples = []
+        self.power = []
         self.max_mhz = None
         self._stop = None
         self._thread = None
@@ -126,6 +127,7 @@ class ClockSampler:
                     mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                     r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                     self.samples.append((mhz, [n for n, m in masks if r & m]))
+                    self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1e3)
                 except Exception:
                     pass
                 self._stop.wait(self.period)
@@ -143,8 +145,12 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         reasons = sorted({n for _, rs in self.samples for n in rs})
-        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 5 ms"}
+        out = {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": reasons, "samples": len(self.samples), "source": "nvml, 5 ms"}
+        if self.power:
+            out["power_w_median"] = round(statistics.median(self.power), 1)
+            out["power_w_max"] = round(max(self.power), 1)
+        return out
 
 
 # ------------------------------------------------------------------------------------------------
@@ -499,7 +505,10 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
     l2_bclk = None
     l2_tbs = (gathered + a_image) / (sum(per_kernel.values()) * 1e-3) / 1e12
     ceiling = None if args.no_extras else gather_ceiling()
-    binding = {"resource": "L2->SMEM gather fill (cp.async, 16 B per lane)",
+    pair_up = per_kernel_image.get("up") == "groups"
+    binding = {"resource": ("chip power cap (1 kW) under sustained load -- the tensor pipe's operand-dependent "
+                            "energy; L2->SMEM fill below its cap (profiles/r02_pair.txt sections 5, 9, 10)")
+               if pair_up else "L2->SMEM gather fill (cp.async, 16 B per lane)",
                "achieved_tbs": round(l2_tbs, 2)}
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0
     l2_bclk = l2_tbs * 1e12 / (148 * sm_mhz * 1e6)
