@@ -2015,8 +2015,10 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     // streamed variant (k_select_pack2): rows bulk-copied through a ring, 16 rows per CTA; needs
     // 16-byte rows (n % 8 == 0) and a ring of >= 2 rows in ~100 KB (two CTAs per SM)
     const size_t rowb = (size_t)p->n * 2;
-    // ring: 8 rows when they fit in ~100 KB (several CTAs per SM), else 4 or 8 rows in one CTA per SM
-    int nslot = 8 * rowb <= 100 * 1024 ? 8 : 8 * rowb <= 190 * 1024 ? 8 : 4 * rowb <= 190 * 1024 ? 4 : 0;
+    // ring: 8 rows when they fit next to the tile's gather indices in 200 KB, else 4 (the 4096 x 11008
+    // down projection: 8 x 22 KB rows + 44 KB of indices do not fit -- 4 slots keep it on this kernel)
+    const size_t idx_bytes = (size_t)round_up(kp_cap * 4, 16);
+    int nslot = 8 * rowb + idx_bytes <= 200 * 1024 ? 8 : 4 * rowb + idx_bytes <= 200 * 1024 ? 4 : 0;
 #ifdef HINM_EXPERIMENTS
     if (const char* e = getenv("HINM_SP2_SLOTS")) nslot = atoi(e);
 #endif

@@ -25,7 +25,7 @@ for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
     so = np.random.default_rng(2).permutation(m)
     cfg = H.HiNMConfig(64, 2, 4, 0.5)
     for _ in range(3):
-        H.compress(W, cfg, so)
+        H.compress(W, cfg, so, groups=False)
     torch.cuda.synchronize()
     wall, stream = [], []
     for _ in range(reps):
@@ -33,7 +33,7 @@ for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e0.record()
-        H.compress(W, cfg, so)
+        H.compress(W, cfg, so, groups=False)
         e1.record()
         torch.cuda.synchronize()
         wall.append(time.perf_counter() - t0)
@@ -41,7 +41,7 @@ for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        H.compress(W, cfg, so)
+        H.compress(W, cfg, so, groups=False)
     e1.record()
     torch.cuda.synchronize()
     b2b = e0.elapsed_time(e1) / reps
@@ -49,11 +49,11 @@ for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
-        H.compress(W, cfg, so)
+        H.compress(W, cfg, so, groups=False)
     torch.cuda.current_stream().wait_stream(s)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, capture_error_mode="relaxed"):
-        pack_g = H.compress(W, cfg, so)
+        pack_g = H.compress(W, cfg, so, groups=False)
     graph.replay()
     torch.cuda.synchronize()
     gt = []
@@ -65,7 +65,7 @@ for name, m, n in (("up", 11008, 4096), ("down", 4096, 11008)):
         e1.record()
         torch.cuda.synchronize()
         gt.append(e0.elapsed_time(e1))
-    ref = H.compress(W, cfg, so)
+    ref = H.compress(W, cfg, so, groups=False)
     same = all(torch.equal(getattr(ref, f), getattr(pack_g, f)) for f in ("tile_ptr", "vec_idx", "kept", "nm_pos",
                                                                             "tile_kofs", "tile_eofs"))
     kp = int(ref.tile_kofs[-1])
