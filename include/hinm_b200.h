@@ -236,6 +236,17 @@ int hinm_group_plan(const hinm_pack_t* pack, void* workspace, size_t workspace_b
 int hinm_group_build(const hinm_pack_t* pack, void* workspace, size_t workspace_bytes, hinm_pack_t* g,
                      void* stream);
 
+/*
+ * Weights and programmatic dependent launch: short hinm_spmm_bf16 launches use PDL, and their weight
+ * streams (operand image, gather indices, tile offsets) start during the previous kernel's tail --
+ * only the activation reads and the Y stores wait for it (griddepcontrol.wait).  The immediately
+ * preceding kernel on the stream must therefore not be one that writes the pack's arrays: every
+ * function here that writes them (hinm_compress_bf16, hinm_pack_build, hinm_group_build) ends with
+ * hinm_stream_fence, a plain one-CTA launch; a caller that writes pack arrays itself (copies,
+ * broadcasts) calls it before the next SpMM.  Async.
+ */
+int hinm_stream_fence(void* stream);
+
 /* Number of kernel launches issued by the most recent hinm_spmm_bf16 call on this thread. */
 int hinm_last_launch_count(void);
 /* Image the most recent hinm_spmm_bf16 call on this thread ran: 0 per-tile, 1 union-group. */

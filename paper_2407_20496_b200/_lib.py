@@ -85,6 +85,7 @@ _SIGNATURES = {
                              c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_size, c_vp], c_int),
     "hinm_last_launch_count": ([], c_int),
     "hinm_last_image": ([], c_int),
+    "hinm_stream_fence": ([c_vp], c_int),
     "hinm_icp_costs": ([c_vp, c_int, c_int, c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "hinm_lex_assignment": ([c_vp, c_int, c_vp], c_int),
     "hinm_ocp_workspace": ([c_int, c_int, c_int, ctypes.POINTER(c_size)], c_int),

@@ -3,6 +3,19 @@
 
 extern "C" const char* hinm_version(void) { return "hinm_b200 0.1.0 (sm_100a)"; }
 
+namespace {
+__global__ void k_stream_fence() {}
+}  // namespace
+
+// A plain (non-PDL) launch after every weight writer: an SpMM launched next with programmatic
+// dependent launch may start streaming its weights during the previous kernel's tail (before
+// griddepcontrol.wait), and that previous kernel is then never the one that wrote them.
+extern "C" int hinm_stream_fence(void* stream) {
+  k_stream_fence<<<1, 32, 0, (cudaStream_t)stream>>>();
+  HINM_LAUNCH_CHECK();
+  return HINM_OK;
+}
+
 extern "C" const char* hinm_status_string(int s) {
   switch (s) {
     case HINM_OK: return "ok";

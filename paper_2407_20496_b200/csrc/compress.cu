@@ -1969,7 +1969,7 @@ extern "C" int hinm_pack_build(hinm_pack_t* p, void* stream_) {
   dim3 gg((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(kmax, 256), 64)), T);
   k_pack_gidx<<<gg, 256, 0, stream>>>(p->tile_ptr, p->tile_kofs, p->vec_idx, p->gidx);
   HINM_LAUNCH_CHECK();
-  return HINM_OK;
+  return hinm_stream_fence(stream_);  // the image's writers are never the kernel right before an SpMM
 }
 
 extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* S, int64_t lds,
@@ -2061,5 +2061,5 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     HINM_CUDA_TRY(cudaMemcpyAsync(p->sigma_o, sigma_o, (size_t)p->m * 4, cudaMemcpyDeviceToDevice,
                                   stream));
   if (p->a_vals && !fused) return hinm_pack_build(p, stream_);
-  return HINM_OK;
+  return hinm_stream_fence(stream_);  // see hinm_pack_build
 }

@@ -521,8 +521,12 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
   // touches only this CTA's shared memory / TMEM, so it overlaps the previous kernel's tail; no
   // global memory is read or written before the previous grid has completed.  The next kernel
   // may start its own prologue as soon as this grid's CTAs start exiting.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Only the roles that touch activations wait for the previous grid (gather: X reads, epilogue:
+  // Y writes); the weight streams (A / metadata, gather indices, unit parameters) start during its
+  // tail -- the previous kernel never writes them (hinm_stream_fence, include/hinm_b200.h).  BERT
+  // and cfg1 shapes under CUDA graphs: 5-12 % per launch (profiles/r02_pair.txt).
+  const bool waits = warp < EPI_WARPS || (warp >= GATHER_WARP0 && !(SPREAD && (warp & 3) == 0));
+  if (!waits) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == AE_WARP) {
     // ============================================================ A / metadata producer
@@ -637,6 +641,8 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
     };
 #pragma unroll
     for (int j = 0; j < PF; ++j) prefetch(j);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // X is the previous kernel's output
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // A row segment is BNT tokens = LPR lanes x 16 B; one warp instruction covers RPI rows.
     // Per-warp constant part of the SWIZZLE_128B destination (row r = gw + GW i: r & 7 = gw & 7)
     constexpr int LPR = BNT / 8, RPI = 32 / LPR;
@@ -790,6 +796,8 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
     //   M=128: row 32q + lane;        chunk c = columns 32c + [0, 32), c in [h NCH, (h+1) NCH)
     // With two accumulators (BNT = 128) the drain of one overlaps the MMAs into the other.
     const int q = warp & 3, h = warp >> 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // Y may still be read by the previous kernel
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (q < n_quads) {
       uint32_t ucount = 0;
       const int r = M64 ? q * 16 + (lane & 15) : q * 32 + lane;

@@ -171,9 +171,23 @@ class DevicePack:
                      "gidx", "a_vals", "a_meta"):
             t = getattr(self, name)
             fields[name] = None if t is None else t.to(device, non_blocking=True)
-        return DevicePack(self.m, self.n, self.V, self.N, self.M, self.total_keep, self.config,
-                          kpad_cap=self.kpad_cap, meta_cap=self.meta_cap, pair=self.pair, rows=self.rows,
-                          group=None if self.group is None else self.group.replicate(device), **fields)
+        rep = DevicePack(self.m, self.n, self.V, self.N, self.M, self.total_keep, self.config,
+                         kpad_cap=self.kpad_cap, meta_cap=self.meta_cap, pair=self.pair, rows=self.rows,
+                         group=None if self.group is None else self.group.replicate(device), **fields)
+        stream_fence(device)
+        return rep
+
+
+def stream_fence(device) -> None:
+    """A plain launch on ``device``'s current stream after writing pack arrays outside the library
+    (copies, broadcasts): the next SpMM may stream its weights during the previous kernel's tail
+    (hinm_stream_fence, include/hinm_b200.h)."""
+    torch = _torch()
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        return
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().hinm_stream_fence(_stream_handle(dev)), "stream_fence")
 
 
 def _alloc_operand_image(pack: DevicePack) -> None:

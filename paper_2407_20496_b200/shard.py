@@ -77,8 +77,13 @@ def broadcast_pack(pack, src: int = 0, group=None, device=None):
         return pack
     m, n, V, N, M, K, kc, mc = meta["scalars"]
     pair, rows = meta["pair"]
-    return DevicePack(m, n, V, N, M, K, meta["config"], kpad_cap=kc, meta_cap=mc, pair=pair, rows=rows,
-                      group=group, **tensors)
+    rep = DevicePack(m, n, V, N, M, K, meta["config"], kpad_cap=kc, meta_cap=mc, pair=pair, rows=rows,
+                     group=group, **tensors)
+    if device is not None and torch.device(device).type == "cuda":
+        from .device import stream_fence
+
+        stream_fence(device)  # the broadcast wrote the pack: fence before the next SpMM
+    return rep
 
 
 def gather_tokens(y_local, tokens: int, group=None, align: int = 8):
