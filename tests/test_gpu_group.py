@@ -171,3 +171,25 @@ def test_replicate_keeps_group():
     a = H.spmm(pack, X, image="groups")
     b = H.spmm(rep, X, image="groups")
     assert torch.equal(a, b)
+
+
+def test_early_weight_streams_after_pack_writers():
+    """Short SpMM launches (PDL) stream their weights before griddepcontrol.wait; every pack writer
+    ends with hinm_stream_fence.  Back-to-back compress -> spmm, rebuild -> spmm and replicate ->
+    spmm sequences on one stream, with the weights changing every iteration, must match the
+    CUDA-core kernel (which reads the reference view, after a synchronize)."""
+    X = torch.as_tensor(synth.randn_bf16((512, 264), 51).astype(np.float32)).cuda().to(torch.bfloat16)
+    for i in range(6):
+        W = torch.as_tensor(synth.randn_bf16((512, 512), 60 + i).astype(np.float32)).cuda().to(torch.bfloat16)
+        so = synth.random_sigma_o(512, 70 + i)
+        pack = H.compress(W, H.HiNMConfig(64, 2, 4, 0.5), so, groups=True)
+        outs = [H.spmm(pack, X, order="original", image=img) for img in ("tiles", "groups")]
+        H.build_group_image(pack)
+        outs.append(H.spmm(pack, X, order="original", image="groups"))
+        rep = pack.replicate("cuda:0")
+        outs.append(H.spmm(rep, X, order="original", image="groups"))
+        torch.cuda.synchronize()
+        ref = H.spmm_simt(pack, X, order="original")
+        for Y in outs:
+            err = (Y.float() - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
+            assert err < 1e-2, (i, err)
