@@ -29,6 +29,7 @@ constexpr int GR = 256;       // rows per group (CTA pair x 128 TMEM lanes)
 constexpr int MW = GR / 32;   // 32-bit mask words per column
 constexpr int GT = 256;       // threads of the greedy CTA
 constexpr int EMAX = 1024;    // open-list entries (live open chunks measured <= 786 at n = 11008)
+static_assert(EMAX == 4 * 256, "the first-fit scan gives each of the 256 threads 4 contiguous entries");
 
 struct Ws {
   size_t inv, mask, cols, nch, err, total;
@@ -141,17 +142,26 @@ __global__ void __launch_bounds__(GT, 1) k_greedy(const uint32_t* __restrict__ m
       uint32_t mm[MW];
 #pragma unroll
       for (int w = 0; w < MW; ++w) mm[w] = bm[i][w];
+      // each thread checks its 4 contiguous entries with 16-byte loads (EMAX = 4 * GT): the lowest
+      // fitting entry of the lowest thread is the first fit
       const int L = s_nlist;
       int mine = INT_MAX;
-      for (int e = tid; e < L; e += GT) {
-        if (cnt[e] >= 4) continue;
-        uint32_t conf = 0u;
+      const int e0 = tid * 4;
+      if (e0 < L) {
+        const int4 c4 = *reinterpret_cast<const int4*>(cnt + e0);
+        uint4 conf = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int w = 0; w < MW; ++w) conf |= twos[w * EMAX + e] & mm[w];
-        if (conf == 0u) {
-          mine = e;
-          break;
+        for (int w = 0; w < MW; ++w) {
+          const uint4 t4 = *reinterpret_cast<const uint4*>(twos + w * EMAX + e0);
+          conf.x |= t4.x & mm[w];
+          conf.y |= t4.y & mm[w];
+          conf.z |= t4.z & mm[w];
+          conf.w |= t4.w & mm[w];
         }
+        if (c4.x < 4 && conf.x == 0u) mine = e0;
+        else if (e0 + 1 < L && c4.y < 4 && conf.y == 0u) mine = e0 + 1;
+        else if (e0 + 2 < L && c4.z < 4 && conf.z == 0u) mine = e0 + 2;
+        else if (e0 + 3 < L && c4.w < 4 && conf.w == 0u) mine = e0 + 3;
       }
       mine = __reduce_min_sync(0xffffffffu, mine);
       if (lane == 0 && mine != INT_MAX) atomicMin(&s_best[it & 1], mine);
