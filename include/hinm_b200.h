@@ -102,6 +102,9 @@ typedef struct hinm_pack_s {
   struct hinm_pack_s* group;
   int32_t pair;
   int32_t rows;
+  /* image choice of hinm_spmm_bf16 for this pack: 0 = the faster for the call, 1 = per-tile only,
+   * 2 = union-group (when `group` is set) */
+  int32_t image;
 } hinm_pack_t;
 
 const char* hinm_version(void);
@@ -170,8 +173,9 @@ int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* saliency, i
  * in TMEM, bf16 out.  Rows of Y in sigma_o order (HINM_ORDER_SIGMA, == hinm_spmm) or original
  * channel order (HINM_ORDER_ORIGINAL, == restore_row_order(hinm_spmm)).  Requires the operand
  * image, B % 8 == 0, ldx % 8 == 0, ldy % 8 == 0, 16-byte aligned X/Y.  With a union-group image
- * attached (pack->group) the faster image for B tokens runs; a union-group pseudo pack passed
- * directly always runs on the CTA-pair kernel.  Async.
+ * attached (pack->group) the image pack->image selects runs (default: the faster one for B tokens;
+ * the two images differ only in fp32 summation order); a union-group pseudo pack passed directly
+ * always runs on the CTA-pair kernel.  Async.
  */
 int hinm_spmm_bf16(const hinm_pack_t* pack, const uint16_t* X, int64_t ldx, int B,
                    uint16_t* Y, int64_t ldy, int out_order, void* stream);

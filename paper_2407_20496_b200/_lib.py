@@ -50,7 +50,9 @@ PackStruct._fields_ = [
     ("tile_kofs", c_vp), ("tile_eofs", c_vp), ("gidx", c_vp), ("a_vals", c_vp),
     ("a_meta", c_vp),
     ("group", ctypes.POINTER(PackStruct)), ("pair", ctypes.c_int32), ("rows", ctypes.c_int32),
+    ("image", ctypes.c_int32),
 ]
+IMAGE_AUTO, IMAGE_TILES, IMAGE_GROUPS = 0, 1, 2
 
 
 class ChainStep(ctypes.Structure):

@@ -1192,7 +1192,8 @@ extern "C" int hinm_spmm_bf16(const hinm_pack_t* pk, const uint16_t* X, int64_t 
   const int variant = kn.variant;
   const int dev = current_device();
   const int sms = sm_count(dev);
-  if (variant == 0 && !kn.xblk && choose_group(pk, B, sms))
+  const bool has_group = pk->group && pk->group->pair && pk->group->a_vals;
+  if (variant == 0 && !kn.xblk && pk->image != 1 && has_group && (pk->image == 2 || choose_group(pk, B, sms)))
     return spmm_pair(pk->group, X, ldx, B, Y, ldy, out_order, prm.y_align32, (cudaStream_t)stream);
   // 128-token units only when 256-token units would leave more than half the SMs idle (e.g. the
   // down projection at 256 tokens per GPU under 8-way token sharding: 64 units -> 128 units,

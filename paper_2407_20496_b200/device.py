@@ -410,6 +410,31 @@ def build_group_image(pack: DevicePack) -> DevicePack:
     return g
 
 
+_IMAGES = {"auto": _lib.IMAGE_AUTO, "tiles": _lib.IMAGE_TILES, "groups": _lib.IMAGE_GROUPS}
+
+
+def image_struct(pack: DevicePack, image: str = "auto"):
+    """The pack's C view with its image choice set (``'auto'`` | ``'tiles'`` | ``'groups'``);
+    the variants are cached next to the pack's own struct."""
+    if image not in _IMAGES:
+        raise ValueError(f"image must be 'auto', 'tiles' or 'groups', got {image!r}")
+    base = pack.struct()
+    if image == "auto":
+        return base
+    if image == "groups" and pack.group is None:
+        raise ValueError("pack has no union-group image (build_group_image)")
+    cache = pack.__dict__.get("_image_structs")
+    if cache is None or cache[0] is not base:
+        cache = (base, {})
+        object.__setattr__(pack, "_image_structs", cache)
+    st = cache[1].get(image)
+    if st is None:
+        st = _lib.PackStruct.from_buffer_copy(base)
+        st.image = _IMAGES[image]
+        cache[1][image] = st
+    return st
+
+
 def spmm(pack: DevicePack, X, out=None, order: str = "sigma", image: str = "auto"):
     """tcgen05 HiNM SpMM: Y (m x B, bf16) = W_hinm @ X (n x B, bf16, channel-major).
 
@@ -438,22 +463,7 @@ def spmm(pack: DevicePack, X, out=None, order: str = "sigma", image: str = "auto
         raise ValueError(f"out must be a ({pack.m}, {B}) bfloat16 tensor on {X.device} with "
                          "contiguous rows")
     ordv = _lib.HINM_ORDER_ORIGINAL if order == "original" else _lib.HINM_ORDER_SIGMA
-    if image == "auto":
-        st = pack.struct()
-    elif image == "groups":
-        if pack.group is None:
-            raise ValueError("pack has no union-group image (build_group_image)")
-        st = pack.group.struct()
-    elif image == "tiles":
-        st = pack.__dict__.get("_tiles_struct")
-        base = pack.struct()
-        if st is None or st._base is not base:
-            st = _lib.PackStruct.from_buffer_copy(base)
-            st.group = None
-            st._base = base
-            object.__setattr__(pack, "_tiles_struct", st)
-    else:
-        raise ValueError(f"image must be 'auto', 'tiles' or 'groups', got {image!r}")
+    st = image_struct(pack, image)
     lib = _lib.load()
     dev = X.device.index
     if dev != torch.cuda.current_device():
@@ -496,9 +506,10 @@ class HostChain:
     buffer copied back to the host.  Tokens run in chunks of ``chunk`` with H2D / SpMM / D2H of
     consecutive chunks overlapped on three streams; the device workspace (3 chunk slots) is
     allocated once here.  Host tensors should be pinned (``pin_memory()``) for the overlap.
+    ``image`` fixes the operand image of every step (default: per call, as :func:`spmm`).
     """
 
-    def __init__(self, steps, out_buf: int, chunk: int = 2048, device=None):
+    def __init__(self, steps, out_buf: int, chunk: int = 2048, device=None, image: str = "auto"):
         torch = _torch()
         if not steps:
             raise ValueError("empty chain")
@@ -513,7 +524,7 @@ class HostChain:
             raise ValueError("chain buffers must be numbered 0..nbuf-1 with 0 the input")
         self.nbuf, self.out_buf, self.chunk = nbuf, out_buf, chunk
         self.buf_rows = (ctypes.c_int64 * nbuf)(*[rows[b] for b in range(nbuf)])
-        self._structs = [p.struct() for p, _, _, _ in steps]
+        self._structs = [image_struct(p, image) for p, _, _, _ in steps]
         self._packs = [p for p, _, _, _ in steps]
         self.steps = (_lib.ChainStep * len(steps))()
         for i, (_, src, dst, order) in enumerate(steps):

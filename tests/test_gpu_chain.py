@@ -1,8 +1,9 @@
 """GPU: the end-to-end host-buffer chain (hinm_chain_run_host) against the device path.
 
-Chunking the tokens does not change any token's accumulation order, so the chain's output must
-be bit-identical to the device SpMMs on the whole batch; the device path itself is checked
-against the oracle in test_gpu_parity.py.  Covers ragged chunks, a two-layer chain with the
+Chunking the tokens does not change any token's accumulation order, so with the operand image
+fixed (per-tile or union-group) the chain's output must be bit-identical to the device SpMMs on
+the whole batch; the device path itself is checked against the oracle in test_gpu_parity.py and
+test_gpu_group.py.  Covers ragged chunks, a two-layer chain with the
 sigma_o restore fused, SIGMA order, and the argument checks.
 """
 
@@ -33,13 +34,14 @@ def test_chain_matches_device_path(B, chunk):
     gate = _pack(512, 256, 20)
     down = _pack(256, 512, 30)
     X = torch.as_tensor(synth.randn_bf16((256, B), 5)).to(torch.bfloat16)
-    chain = H.HostChain([(gate, 0, 1, "original"), (up, 0, 2, "original"),
-                         (down, 2, 3, "original")], out_buf=3, chunk=chunk)
-    Yh = chain.run(X.pin_memory())
-    torch.cuda.synchronize()
-    Xd = X.cuda()
-    ref = H.spmm(down, H.spmm(up, Xd, order="original"), order="original")
-    assert torch.equal(Yh, ref.cpu())
+    for image in ("tiles", "groups"):  # the image is fixed: per-call choices could differ per chunk
+        chain = H.HostChain([(gate, 0, 1, "original"), (up, 0, 2, "original"),
+                             (down, 2, 3, "original")], out_buf=3, chunk=chunk, image=image)
+        Yh = chain.run(X.pin_memory())
+        torch.cuda.synchronize()
+        Xd = X.cuda()
+        ref = H.spmm(down, H.spmm(up, Xd, order="original", image=image), order="original", image=image)
+        assert torch.equal(Yh, ref.cpu()), image
 
 
 def test_chain_sigma_order_and_unpinned_host():
