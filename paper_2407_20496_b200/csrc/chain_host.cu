@@ -17,7 +17,10 @@
 
 namespace {
 
-constexpr int NSLOT = 3;
+#ifndef HINM_CHAIN_SLOTS
+#define HINM_CHAIN_SLOTS 3
+#endif
+constexpr int NSLOT = HINM_CHAIN_SLOTS;
 
 struct CopyStreams {
   cudaStream_t h2d = nullptr, d2h = nullptr;
