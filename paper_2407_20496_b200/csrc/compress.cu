@@ -15,11 +15,34 @@
 //   k_nm_select(_rows), k_pack_*   a8/a10 general N:M / V path and HiNMEncoding -> operand image
 #include <climits>
 #include <cstdlib>
+#include <utility>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
 
 namespace hinm {
+
+// Programmatic dependent launch over the compressor's chain of dependent kernels (launch_chain
+// below): each kernel waits for its predecessor grid before it touches memory and lets its
+// successor launch at once, so a launch's latency and CTA ramp overlap the predecessor's tail.
+// Launched without the attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// The budget select's histogram / candidate count and key OR / AND words, zeroed by the first CTA
+// of the score kernel (instead of three memset nodes between launches).
+struct BselInit {
+  uint32_t* ghist;               // BSEL_BINS + 4 words
+  unsigned long long* keybits;   // [0] = OR of keys (0), [1] = AND of keys (~0)
+  __device__ __forceinline__ void run() const {
+    if (blockIdx.x | blockIdx.y) return;
+    for (int i = threadIdx.x; i < kBselWords; i += blockDim.x) ghist[i] = 0u;
+    if (threadIdx.x == 0) { keybits[0] = 0ull; keybits[1] = ~0ull; }
+  }
+  static constexpr int kBselWords = (1 << 12) + 4;
+};
 
 struct Src {
   const uint16_t* W;
@@ -39,7 +62,9 @@ struct Src {
 // a3: column scores.  numpy reduces axis 0 of the (V, n) gathered block row by row (sequential)
 // for n >= 2; for n == 1 the operand is contiguous and numpy uses pairwise summation.
 __global__ void k_scores(Src src, const int32_t* __restrict__ sigma_o, int n, int V,
-                         double* __restrict__ scores) {
+                         double* __restrict__ scores, BselInit init) {
+  pdl_enter();
+  init.run();
   const int t = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -62,8 +87,10 @@ __global__ void k_scores(Src src, const int32_t* __restrict__ sigma_o, int n, in
 template <int NT>
 __global__ void __launch_bounds__(NT) k_scores4(const uint16_t* __restrict__ W, int64_t ldw,
                                                 const int32_t* __restrict__ sigma_o, int n, int V,
-                                                double* __restrict__ scores) {
+                                                double* __restrict__ scores, BselInit init) {
   extern __shared__ int32_t s_rows[];
+  pdl_enter();
+  init.run();
   const int t = blockIdx.y;
   for (int r = threadIdx.x; r < V; r += NT) s_rows[r] = sigma_o[(int64_t)t * V + r];
   __syncthreads();
@@ -102,8 +129,10 @@ __global__ void __launch_bounds__(NT) k_scores4(const uint16_t* __restrict__ W, 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, int64_t ldw,
                                                 const int32_t* __restrict__ sigma_o, int n, int V,
-                                                double* __restrict__ scores) {
+                                                double* __restrict__ scores, BselInit init) {
   extern __shared__ int32_t s_rows8[];
+  pdl_enter();
+  init.run();
   const int t = blockIdx.y;
   for (int r = threadIdx.x; r < V; r += NT) s_rows8[r] = sigma_o[(int64_t)t * V + r];
   __syncthreads();
@@ -373,6 +402,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT, rank_min_blocks<NT>()) k_tile_rank(
     const double* __restrict__ scores, int n, int P, int M, int G, double* __restrict__ gains,
     uint16_t* __restrict__ order16, unsigned long long* __restrict__ keybits) {
+  pdl_enter();
   constexpr int NB = RANK_PER * NT;
   extern __shared__ __align__(16) uint8_t rk_smem[];
   uint64_t* key = reinterpret_cast<uint64_t*>(rk_smem);                      // [n] keys, then sorted
@@ -530,6 +560,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict__ order16, int n,
                                                       const int32_t* __restrict__ tile_ptr,
                                                       int32_t* __restrict__ surv, uint8_t* __restrict__ vmask) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t sv_flags[];
   typedef cub::BlockScan<int, NT> BS;
   __shared__ typename BS::TempStorage scan_tmp;
@@ -720,6 +751,7 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
 // exact key among the candidates (block radix sort when they fit, else radix select over the
 // list), finds every tile's bounds around it and applies the (q, t) tie order (budget_tail).
 constexpr int BSEL_BITS = 12, BSEL_BINS = 1 << BSEL_BITS, BSEL_CAP = 4096;
+static_assert(BselInit::kBselWords == BSEL_BINS + 4, "BselInit zeroes the histogram and the candidate count");
 
 struct BselShape {
   int shift;        // the bin digit = key bits [shift, shift + BSEL_BITS)
@@ -739,6 +771,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_bsel_hist(const double* __restrict__ gains, int64_t total,
                                                   const unsigned long long* __restrict__ keybits,
                                                   uint32_t* __restrict__ ghist) {
+  pdl_enter();
   __shared__ uint32_t hist[BSEL_BINS];
   const int lane = threadIdx.x & 31;
   const BselShape sh = bsel_shape(keybits);
@@ -789,6 +822,7 @@ __global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ 
                                                      const uint32_t* __restrict__ ghist,
                                                      unsigned long long* __restrict__ cand,
                                                      unsigned int* __restrict__ ncand) {
+  pdl_enter();
   __shared__ int s_bin;
   __shared__ int64_t s_k;
   const int lane = threadIdx.x & 31;
@@ -820,6 +854,7 @@ __global__ void __launch_bounds__(NT) k_bsel_pick(const double* __restrict__ gai
                                                   const unsigned long long* __restrict__ cand,
                                                   const unsigned int* __restrict__ ncand,
                                                   unsigned long long* __restrict__ xsel) {
+  pdl_enter();
   __shared__ uint64_t s_cand[BSEL_CAP];
   __shared__ uint64_t s_x;
   __shared__ int s_bin;
@@ -881,6 +916,7 @@ __global__ void __launch_bounds__(NT) k_bsel_pick(const double* __restrict__ gai
 __global__ void __launch_bounds__(256) k_bsel_bounds(const double* __restrict__ gains, int T, int G,
                                                      const unsigned long long* __restrict__ xsel,
                                                      int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr) {
+  pdl_enter();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (t >= T) return;
   const uint64_t x = __ldcg(xsel);
@@ -902,6 +938,7 @@ __global__ void __launch_bounds__(NT) k_bsel_tail(const double* __restrict__ gai
                                                   const unsigned long long* __restrict__ xsel,
                                                   int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
                                                   int32_t* __restrict__ tile_ptr) {
+  pdl_enter();
   budget_tail<NT>(gains, T, G, total_groups, M, __ldcg(xsel), false, lo_scr, hi_scr, tile_ptr);
 }
 
@@ -1178,6 +1215,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_pack_offsets(const int32_t* __restrict__ tile_ptr, int T,
                                                      int32_t* __restrict__ kofs,
                                                      int32_t* __restrict__ eofs) {
+  pdl_enter();
   typedef cub::BlockScan<int, NT> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int carry_k, carry_e;
@@ -1319,6 +1357,7 @@ __global__ void __launch_bounds__(NT) k_select_pack(
     const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
     uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
     uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t sp_smem[];
   const int t = blockIdx.y, r0 = blockIdx.x * R;
   const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
@@ -1461,6 +1500,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
     uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
     uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
+  pdl_enter();
   constexpr int NC = 32 * SP2_CWARPS;
   extern __shared__ __align__(128) uint8_t sp2_smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], idx_bar;
@@ -1624,6 +1664,31 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
 namespace hinm {
 namespace {
 
+// One kernel of the compressor's dependent chain (kernels that begin with pdl_enter()), launched
+// with programmatic stream serialization.
+inline bool chain_pdl() {
+#ifdef HINM_EXPERIMENTS
+  static const int on = [] { const char* e = getenv("HINM_COMPRESS_PDL"); return e && e[0] == '0' ? 0 : 1; }();
+  return on;
+#else
+  return true;
+#endif
+}
+template <typename... P, typename... A>
+cudaError_t launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, A&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = chain_pdl() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 struct WsLayout {
   size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, err, ghist, cub, total;
 };
@@ -1711,10 +1776,10 @@ int launch_tile_rank(const double* scores, int n, int T, int M, int G, double* g
     // dynamic + static shared memory may pass 48 KB while the dynamic part alone does not: opt in
     // with slack for the static part
     HINM_CUDA_TRY(smem_optin((const void*)k_tile_rank<512>, (int)smem + 4096));
-    k_tile_rank<512><<<T, 512, smem, stream>>>(scores, n, P, M, G, gains, order16, keybits);
+    HINM_CUDA_TRY(launch_chain(k_tile_rank<512>, T, 512, smem, stream, scores, n, P, M, G, gains, order16, keybits));
   } else {
     HINM_CUDA_TRY(smem_optin((const void*)k_tile_rank<1024>, (int)smem + 4096));
-    k_tile_rank<1024><<<T, 1024, smem, stream>>>(scores, n, P, M, G, gains, order16, keybits);
+    HINM_CUDA_TRY(launch_chain(k_tile_rank<1024>, T, 1024, smem, stream, scores, n, P, M, G, gains, order16, keybits));
   }
   HINM_LAUNCH_CHECK();
   return HINM_OK;
@@ -1777,27 +1842,25 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   double* gains = (double*)(ws + L.gains);
   Src src{W, ldw, Wd, ldwd, S, lds};
 
+  uint32_t* ghist = (uint32_t*)(ws + L.ghist);
+  unsigned long long* keybits = (unsigned long long*)(ghist + BSEL_BINS + 4 + 2 * BSEL_CAP);
+  const BselInit init{ghist, keybits};  // zeroed by the score kernel's first CTA
   if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
-    k_scores8<128><<<dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream>>>(
-        W, ldw, sigma_o, n, V, scores);
+    HINM_CUDA_TRY(launch_chain(k_scores8<128>, dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream,
+                               W, ldw, sigma_o, n, V, scores, init));
   } else if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
-    k_scores4<128><<<dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream>>>(
-        W, ldw, sigma_o, n, V, scores);
+    HINM_CUDA_TRY(launch_chain(k_scores4<128>, dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream,
+                               W, ldw, sigma_o, n, V, scores, init));
   } else {
-    k_scores<<<dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream>>>(src, sigma_o, n, V, scores);
+    HINM_CUDA_TRY(launch_chain(k_scores, dim3((unsigned)ceil_div(n, 256), T), 256, 0, stream, src, sigma_o, n, V,
+                               scores, init));
   }
-  HINM_LAUNCH_CHECK();
   const int64_t Tn = (int64_t)T * n;
   if (n > 16384) {  // payload / offsets of the device-wide segmented sort
     k_iota_cols<<<(unsigned)ceil_div(Tn, 256), 256, 0, stream>>>(vals_in, n, Tn);
     k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
     HINM_LAUNCH_CHECK();
   }
-  uint32_t* ghist = (uint32_t*)(ws + L.ghist);
-  unsigned long long* keybits = (unsigned long long*)(ghist + BSEL_BINS + 4 + 2 * BSEL_CAP);
-  HINM_CUDA_TRY(cudaMemsetAsync(ghist, 0, BSEL_BINS * 4 + 16, stream));
-  HINM_CUDA_TRY(cudaMemsetAsync(keybits, 0, 8, stream));
-  HINM_CUDA_TRY(cudaMemsetAsync(keybits + 1, 0xFF, 8, stream));
   int P2 = 2;
   while (P2 < n) P2 <<= 1;
   const bool fused = n <= 16384 && G > 0 && tile_rank_smem(n, P2) <= 220 * 1024;
@@ -1843,19 +1906,21 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
       // atomics and scans the global one, so 2 x SMs CTAs spent their time on those fixed costs
       unsigned long long* xsel = keybits + 2;
       const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms / 4, ceil_div(total, 4096)));
-      k_bsel_hist<1024><<<nblk, 1024, 0, stream>>>(gains, total, keybits, ghist);
-      k_bsel_collect<1024><<<nblk, 1024, 0, stream>>>(gains, total, groups, keybits, ghist, cand, ncand);
-      k_bsel_pick<512><<<1, 512, 0, stream>>>(gains, T, G, groups, keybits, ghist, cand, ncand, xsel);
-      k_bsel_bounds<<<(unsigned)ceil_div(T, 8), 256, 0, stream>>>(gains, T, G, xsel, lo_s, hi_s);
-      k_bsel_tail<512><<<1, 512, 0, stream>>>(gains, T, G, groups, M, xsel, lo_s, hi_s, tile_ptr);
-      HINM_LAUNCH_CHECK();
+      HINM_CUDA_TRY(launch_chain(k_bsel_hist<1024>, nblk, 1024, 0, stream, gains, total, keybits, ghist));
+      HINM_CUDA_TRY(launch_chain(k_bsel_collect<1024>, nblk, 1024, 0, stream, gains, total, groups, keybits, ghist,
+                                 cand, ncand));
+      HINM_CUDA_TRY(launch_chain(k_bsel_pick<512>, 1, 512, 0, stream, gains, T, G, groups, keybits, ghist, cand,
+                                 ncand, xsel));
+      HINM_CUDA_TRY(launch_chain(k_bsel_bounds, (unsigned)ceil_div(T, 8), 256, 0, stream, gains, T, G, xsel, lo_s,
+                                 hi_s));
+      HINM_CUDA_TRY(launch_chain(k_bsel_tail<512>, 1, 512, 0, stream, gains, T, G, groups, M, xsel, lo_s, hi_s,
+                                 tile_ptr));
     }
   }
   if (fused) {
     const size_t fsm = (size_t)round_up(n, 16);
     HINM_CUDA_TRY(smem_optin((const void*)k_survivors_ord<512>, (int)fsm + 4096));
-    k_survivors_ord<512><<<T, 512, fsm, stream>>>(order16, n, tile_ptr, surv, vector_mask);
-    HINM_LAUNCH_CHECK();
+    HINM_CUDA_TRY(launch_chain(k_survivors_ord<512>, T, 512, fsm, stream, order16, n, tile_ptr, surv, vector_mask));
     return HINM_OK;
   }
   const size_t smem = (size_t)n;
@@ -2010,8 +2075,8 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     int64_t kcap = 0, mcap = 0, acap = 0;
     hinm_pack_capacity(p->m, p->n, p->V, p->total_keep, &kcap, &mcap, &acap);
     if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
-    k_pack_offsets<256><<<1, 256, 0, stream>>>(tptr, p->T, p->tile_kofs, p->tile_eofs);
-    HINM_LAUNCH_CHECK();
+    HINM_CUDA_TRY(launch_chain(k_pack_offsets<256>, 1, 256, 0, stream, (const int32_t*)tptr, p->T, p->tile_kofs,
+                               p->tile_eofs));
     // streamed variant (k_select_pack2): rows bulk-copied through a ring, 16 rows per CTA; needs
     // 16-byte rows (n % 8 == 0) and a ring of >= 2 rows in ~100 KB (two CTAs per SM)
     const size_t rowb = (size_t)p->n * 2;
@@ -2032,15 +2097,16 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
       if (const char* e = getenv("HINM_SP2")) kern = e[0] == '1' ? k_select_pack2<1> : e[0] == '2' ? k_select_pack2<2> : kern;
 #endif
       HINM_CUDA_TRY(smem_optin((const void*)kern, (int)s2 + 4096));
-      kern<<<dim3(p->V / SP2_ROWS, p->T), 32 * (SP2_CWARPS + 1), s2, stream>>>(
-          W, ldw, sigma_o, sp, si, p->n, p->V, nslot, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
-          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+      HINM_CUDA_TRY(launch_chain(kern, dim3(p->V / SP2_ROWS, p->T), 32 * (SP2_CWARPS + 1), s2, stream, W, ldw,
+                                 sigma_o, sp, si, p->n, p->V, nslot, (const int32_t*)p->tile_kofs,
+                                 (const int32_t*)p->tile_eofs, p->nm_pos, p->kept_bf16, p->a_vals,
+                                 (uint32_t*)p->a_meta, p->gidx));
     } else {
       // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory
       HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
-      k_select_pack<256, 4><<<dim3(p->V / 4, p->T), 256, fsmem, stream>>>(
-          W, ldw, sigma_o, sp, si, p->n, p->V, p->tile_kofs, p->tile_eofs, p->nm_pos, p->kept_bf16,
-          p->a_vals, (uint32_t*)p->a_meta, p->gidx);
+      HINM_CUDA_TRY(launch_chain(k_select_pack<256, 4>, dim3(p->V / 4, p->T), 256, fsmem, stream, W, ldw, sigma_o,
+                                 sp, si, p->n, p->V, (const int32_t*)p->tile_kofs, (const int32_t*)p->tile_eofs,
+                                 p->nm_pos, p->kept_bf16, p->a_vals, (uint32_t*)p->a_meta, p->gidx));
     }
     HINM_LAUNCH_CHECK();
     int rc = HINM_OK;
