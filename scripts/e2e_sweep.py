@@ -41,3 +41,23 @@ for chunk in (1024, 2048, 4096):
                       (packs["down"], 2, 3, "original")], out_buf=3, chunk=chunk, device=dev)
     out[f"e2e_ms_chunk{chunk}"] = round(t(lambda: ch.run(xh, yh)), 4)
 print(json.dumps(out))
+# diagnostics: the chain's compute alone (device buffers, 2048-token chunks) and the copy pipeline alone
+if os.environ.get("E2E_DIAG"):
+    xc = torch.empty(4096, 2048, dtype=torch.bfloat16, device=dev).normal_()
+    def comp():
+        for _ in range(tok // 2048):
+            g = H.spmm(packs["gate"], xc, order="original")
+            u = H.spmm(packs["up"], xc, order="original")
+            H.spmm(packs["down"], u, order="original")
+    out["compute_only_ms_chunk2048"] = round(t(comp), 4)
+    print(json.dumps(out))
+    # the duplex copies alone and with the chain's compute running concurrently on a third stream
+    s3 = torch.cuda.Stream()
+    def duplex_with_compute():
+        with torch.cuda.stream(s3):
+            comp()
+        duplex()
+        torch.cuda.current_stream().wait_stream(s3)
+    out["duplex_plus_compute_ms"] = round(t(duplex_with_compute), 4)
+    out["duplex_ms"] = round(t(duplex), 4)
+    print(json.dumps(out))
