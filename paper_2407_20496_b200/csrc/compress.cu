@@ -559,7 +559,8 @@ __global__ void __launch_bounds__(NT, rank_min_blocks<NT>()) k_tile_rank(
 template <int NT>
 __global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict__ order16, int n,
                                                       const int32_t* __restrict__ tile_ptr,
-                                                      int32_t* __restrict__ surv, uint8_t* __restrict__ vmask) {
+                                                      int32_t* __restrict__ surv, uint8_t* __restrict__ vmask,
+                                                      uint16_t* __restrict__ surv16) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t sv_flags[];
   typedef cub::BlockScan<int, NT> BS;
@@ -578,8 +579,12 @@ __global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict
   int off;
   BS(scan_tmp).ExclusiveSum(cnt, off);
   int32_t* out = surv + b0 + off;
+  uint16_t* out16 = surv16 + (int64_t)t * n + off;  // n <= 16384 on this path
   for (int c = c0; c < c1; ++c)
-    if (sv_flags[c]) *out++ = c;
+    if (sv_flags[c]) {
+      *out++ = c;
+      *out16++ = (uint16_t)c;
+    }
   if (vmask) {
     uint8_t* vm = vmask + (int64_t)t * n;
     for (int j = threadIdx.x; j < n; j += NT) vm[j] = sv_flags[j];
@@ -1488,22 +1493,33 @@ constexpr int SP2_ROWS = 16;
 constexpr int SP2_CWARPS = 8;  // consumer warps; warp 8 is the producer
 
 // Producer warp 8: the tile's gather indices (one bulk copy of the k int32 column ids) and the 16
-// weight rows through the ring, each slot refilled as soon as all consumer warps released it
+// weight rows through the NS-slot ring, each slot refilled as soon as all consumer warps released it
 // (per-slot full / empty mbarriers, no CTA-wide barrier in the loop).  Consumer warps 0-7: rows in
-// quads; warp w takes items w * 32 + lane (+ 256 ...) of the quad, item = (16-K chunk, row pair).
+// quads; a warp takes 32 consecutive 16-K chunks of one row pair of the quad (item = row pair x
+// chunk, warp-uniform row pair: the two row bases are uniform and every load is [offset + base]).
 // DBG (experiments build only, results garbage): 1 = rows streamed, no select / stores; 2 = select and
 // stores on whatever the ring holds, no row copies.
-template <int DBG = 0>
+// A group's four column ids from the tile's index list in shared memory (int32 ids, or uint16 ids
+// when the list is the compressor's own survivors, halving the list's shared-memory footprint).
+__device__ __forceinline__ int4 grp_idx(const int32_t* s, int g) { return reinterpret_cast<const int4*>(s)[g]; }
+__device__ __forceinline__ int4 grp_idx(const uint16_t* s, int g) {
+  const uint2 v = reinterpret_cast<const uint2*>(s)[g];
+  return make_int4((int)(v.x & 0xFFFFu), (int)(v.x >> 16), (int)(v.y & 0xFFFFu), (int)(v.y >> 16));
+}
+
+// sig_idx: tile t's ids at sig_idx + sig_ptr[t] (idx_stride == 0) or at sig_idx + t * idx_stride.
+template <int DBG = 0, int NS = 8, typename IDX = int32_t>
 __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
-    const int32_t* __restrict__ sig_ptr, const int32_t* __restrict__ sig_idx, int n, int V, int nslot,
+    const int32_t* __restrict__ sig_ptr, const IDX* __restrict__ sig_idx, int idx_stride, int n, int V,
     const int32_t* __restrict__ kofs_g, const int32_t* __restrict__ eofs_g,
     uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
     uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
+  static_assert(NS % 4 == 0 && NS <= 16, "the ring holds whole quads of rows");
   pdl_enter();
   constexpr int NC = 32 * SP2_CWARPS;
   extern __shared__ __align__(128) uint8_t sp2_smem[];
-  __shared__ __align__(8) uint64_t full[16], empty[16], idx_bar;
+  __shared__ __align__(8) uint64_t full[NS], empty[NS], idx_bar;
   const int t = blockIdx.y, r0 = blockIdx.x * SP2_ROWS;
   const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
   const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
@@ -1512,13 +1528,13 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)n * 2;  // host: n % 8 == 0
   uint8_t* s_rows = sp2_smem;
-  int32_t* s_idx = reinterpret_cast<int32_t*>(sp2_smem + (size_t)nslot * row_bytes);
+  IDX* s_idx = reinterpret_cast<IDX*>(sp2_smem + (size_t)NS * row_bytes);
   const uint32_t rows_u32 = (uint32_t)__cvta_generic_to_shared(s_rows);
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(full);
   const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(empty);
   const uint32_t ibar = (uint32_t)__cvta_generic_to_shared(&idx_bar);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nslot; ++i) {
+    for (int i = 0; i < NS; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * i));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(SP2_CWARPS));
     }
@@ -1536,14 +1552,16 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
                      "l"(src), "r"(bytes), "r"(bar)
                      : "memory");
       };
-      bulk((uint32_t)__cvta_generic_to_shared(s_idx), sig_idx + b, (uint32_t)k * 4, ibar);  // k % 4 == 0
+      // k % 4 == 0; a uint16 list is read to the next 16 bytes (inside the tile's n-stride slot)
+      const IDX* src = sig_idx + (idx_stride ? (int64_t)t * idx_stride : (int64_t)b);
+      bulk((uint32_t)__cvta_generic_to_shared(s_idx), src, ((uint32_t)k * (uint32_t)sizeof(IDX) + 15u) & ~15u, ibar);
       int32_t rows[SP2_ROWS];
 #pragma unroll
       for (int i = 0; i < SP2_ROWS; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
 #pragma unroll
       for (int rr = 0; rr < SP2_ROWS; ++rr) {
         if (rr >= nrows) break;
-        const int slot = rr % nslot, use = rr / nslot;
+        const int slot = rr % NS, use = rr / NS;
         if (use > 0) {
           sp_mbar_wait(empty0 + 8 * slot, (use - 1) & 1);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
@@ -1563,23 +1581,27 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
   const int64_t ref_base = (int64_t)V * (b / 4) * 2;
   const int nch = kp / 16;        // 16-K chunks with values
   const int nch_meta = nblk * 8;  // chunks covered by metadata blocks (>= nch)
+  const int nch_pad = (nch_meta + 31) & ~31;
   const int nfull = G / 4;        // chunks whose 4 groups are all real
   uint16_t* meta16 = reinterpret_cast<uint16_t*>(a_meta + (int64_t)eofs * V * 4);
-  const int4* s_idx4 = reinterpret_cast<const int4*>(s_idx);
   for (int rq = 0; rq < nrows; rq += 4) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sp_mbar_wait(full0 + 8 * ((rq + q) % nslot), ((rq + q) / nslot) & 1);
-    for (int it = warp * 32 + lane; it < (DBG == 1 ? 0 : nch_meta * 2); it += NC) {
-      const int ch = it >> 1, rr = rq + 2 * (it & 1), r = r0 + rr;  // rows r, r + 1
-      const uint16_t* rowA = reinterpret_cast<const uint16_t*>(s_rows + (size_t)(rr % nslot) * row_bytes);
-      const uint16_t* rowB = reinterpret_cast<const uint16_t*>(s_rows + (size_t)((rr + 1) % nslot) * row_bytes);
+    for (int q = 0; q < 4; ++q) sp_mbar_wait(full0 + 8 * ((rq + q) % NS), ((rq + q) / NS) & 1);
+    // iw: the warp's first item (warp-uniform); items [0, nch_pad) are row pair 0, [nch_pad, 2 nch_pad) pair 1
+    for (int iw = warp * 32; iw < (DBG == 1 ? 0 : 2 * nch_pad); iw += NC) {
+      const int half = iw >= nch_pad ? 1 : 0;
+      const int ch = iw - half * nch_pad + lane;
+      if (ch >= nch_meta) continue;
+      const int rr = rq + 2 * half, r = r0 + rr;  // rows r, r + 1 (warp-uniform)
+      const uint16_t* rowA = reinterpret_cast<const uint16_t*>(s_rows + (size_t)(rr % NS) * row_bytes);
+      const uint16_t* rowB = reinterpret_cast<const uint16_t*>(s_rows + (size_t)((rr + 1) % NS) * row_bytes);
       const int g0 = ch * 4;
       uint32_t pa[4], va[4], pb[4], vb[4], ba = 0, bb = 0;
       if (ch < nfull) {
         // all four groups real: every shared-memory load of the chunk issued before any compare
         int4 i4[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) i4[c] = s_idx4[g0 + c];
+        for (int c = 0; c < 4; ++c) i4[c] = grp_idx(s_idx, g0 + c);
         uint32_t av[16], bv[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1603,7 +1625,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
         for (int c = 0; c < 4; ++c) {
           const int g = g0 + c;
           if (g < G) {
-            const int4 i4 = s_idx4[g];
+            const int4 i4 = grp_idx(s_idx, g);
             const uint32_t a0 = rowA[i4.x], a1 = rowA[i4.y], a2 = rowA[i4.z], a3 = rowA[i4.w];
             const uint32_t b0 = rowB[i4.x], b1 = rowB[i4.y], b2 = rowB[i4.z], b3 = rowB[i4.w];
             uint32_t mA, mB, nb;
@@ -1652,7 +1674,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     __syncwarp();
     if (lane == 0)
       for (int q = 0; q < 4; ++q)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * ((rq + q) % nslot)) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * ((rq + q) % NS)) : "memory");
   }
 }
 
@@ -1690,7 +1712,7 @@ cudaError_t launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cu
 }
 
 struct WsLayout {
-  size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, err, ghist, cub, total;
+  size_t scores, sorted, vals_in, order, offsets, gains, lo, hi, surv_tmp, surv16, err, ghist, cub, total;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1721,6 +1743,7 @@ int ws_layout(int m, int n, int V, int M, WsLayout* L) {
   L->lo = take(4 * T);
   L->hi = take(4 * T);
   L->surv_tmp = take(4 * Tn);  // survivors when the caller supplies its own sigma_i
+  L->surv16 = take(2 * Tn);    // fused prune path: tile t's survivors as uint16 at t * n (select + pack)
   L->err = take(16);
   // budget select: bin histogram + candidate count, candidate keys, key OR / AND words
   L->ghist = take(BSEL_BINS * 4 + 16 + BSEL_CAP * 8 + 24);  // + key OR / AND words, threshold key
@@ -1783,6 +1806,14 @@ int launch_tile_rank(const double* scores, int n, int T, int M, int G, double* g
   }
   HINM_LAUNCH_CHECK();
   return HINM_OK;
+}
+
+// vector_prune's fused tile-rank path (k_tile_rank + k_survivors_ord): also leaves the survivors as
+// uint16 at t * n in the workspace
+bool prune_fused(int n, int M) {
+  int P2 = 2;
+  while (P2 < n) P2 <<= 1;
+  return n <= 16384 && n / M > 0 && tile_rank_smem(n, P2) <= 220 * 1024;
 }
 
 int status_from_rank(int code, int mask_mode) {
@@ -1861,9 +1892,7 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     k_segment_offsets<<<(unsigned)ceil_div(T + 1, 256), 256, 0, stream>>>(offsets, T, n);
     HINM_LAUNCH_CHECK();
   }
-  int P2 = 2;
-  while (P2 < n) P2 <<= 1;
-  const bool fused = n <= 16384 && G > 0 && tile_rank_smem(n, P2) <= 220 * 1024;
+  const bool fused = prune_fused(n, M);
   uint16_t* order16 = reinterpret_cast<uint16_t*>(sorted);  // fused path: sorted column order (T x n)
   if (fused) {
     int st2 = launch_tile_rank(scores, n, T, M, G, gains, order16, keybits, stream);
@@ -1920,7 +1949,8 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   if (fused) {
     const size_t fsm = (size_t)round_up(n, 16);
     HINM_CUDA_TRY(smem_optin((const void*)k_survivors_ord<512>, (int)fsm + 4096));
-    HINM_CUDA_TRY(launch_chain(k_survivors_ord<512>, T, 512, fsm, stream, order16, n, tile_ptr, surv, vector_mask));
+    HINM_CUDA_TRY(launch_chain(k_survivors_ord<512>, T, 512, fsm, stream, order16, n, tile_ptr, surv, vector_mask,
+                               (uint16_t*)(ws + L.surv16)));
     return HINM_OK;
   }
   const size_t smem = (size_t)n;
@@ -2082,25 +2112,44 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     const size_t rowb = (size_t)p->n * 2;
     // ring: 8 rows when they fit next to the tile's gather indices in 200 KB, else 4 (the 4096 x 11008
     // down projection: 8 x 22 KB rows + 44 KB of indices do not fit -- 4 slots keep it on this kernel)
-    const size_t idx_bytes = (size_t)round_up(kp_cap * 4, 16);
+    // the tile's index list: the compressor's own survivors as uint16 (vector_prune's fused path
+    // leaves them at t * n in the workspace), a caller's sigma_i as int32
+    const bool idx16 = own_sigma && prune_fused(p->n, p->M);
+    const size_t idx_bytes = (size_t)round_up(kp_cap * (idx16 ? 2 : 4), 16);
     int nslot = 8 * rowb + idx_bytes <= 200 * 1024 ? 8 : 4 * rowb + idx_bytes <= 200 * 1024 ? 4 : 0;
 #ifdef HINM_EXPERIMENTS
-    if (const char* e = getenv("HINM_SP2_SLOTS")) nslot = atoi(e);
+    if (const char* e = getenv("HINM_SP2_SLOTS")) nslot = atoi(e) == 4 ? 4 : nslot;
 #endif
-    const size_t s2 = (size_t)nslot * rowb + (size_t)round_up(kp_cap * 4, 16);
+    const size_t s2 = (size_t)nslot * rowb + idx_bytes;
     const bool streamed = (p->n % 8) == 0 && p->n <= 65536 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0 &&
                           nslot >= 4 && p->V % SP2_ROWS == 0 && s2 <= 200 * 1024 &&
                           ((uintptr_t)p->a_vals & 31) == 0 && ((uintptr_t)si & 15) == 0;
     if (streamed) {
-      auto kern = k_select_pack2<0>;
+      const dim3 grid(p->V / SP2_ROWS, p->T), block(32 * (SP2_CWARPS + 1));
+      auto go = [&](auto kern, const auto* idx, int stride) -> int {
+        HINM_CUDA_TRY(smem_optin((const void*)kern, (int)s2 + 4096));
+        HINM_CUDA_TRY(launch_chain(kern, grid, block, s2, stream, W, ldw, sigma_o, sp, idx, stride, p->n, p->V,
+                                   (const int32_t*)p->tile_kofs, (const int32_t*)p->tile_eofs, p->nm_pos,
+                                   p->kept_bf16, p->a_vals, (uint32_t*)p->a_meta, p->gidx));
+        return HINM_OK;
+      };
 #ifdef HINM_EXPERIMENTS
-      if (const char* e = getenv("HINM_SP2")) kern = e[0] == '1' ? k_select_pack2<1> : e[0] == '2' ? k_select_pack2<2> : kern;
+      int dbg = 0;
+      if (const char* e = getenv("HINM_SP2")) dbg = e[0] == '1' ? 1 : e[0] == '2' ? 2 : 0;
 #endif
-      HINM_CUDA_TRY(smem_optin((const void*)kern, (int)s2 + 4096));
-      HINM_CUDA_TRY(launch_chain(kern, dim3(p->V / SP2_ROWS, p->T), 32 * (SP2_CWARPS + 1), s2, stream, W, ldw,
-                                 sigma_o, sp, si, p->n, p->V, nslot, (const int32_t*)p->tile_kofs,
-                                 (const int32_t*)p->tile_eofs, p->nm_pos, p->kept_bf16, p->a_vals,
-                                 (uint32_t*)p->a_meta, p->gidx));
+      const uint16_t* s16 = (const uint16_t*)((const char*)workspace + L.surv16);
+      int rc2;
+#ifdef HINM_EXPERIMENTS
+      if (dbg && idx16)
+        rc2 = nslot == 8 ? (dbg == 1 ? go(k_select_pack2<1, 8, uint16_t>, s16, p->n) : go(k_select_pack2<2, 8, uint16_t>, s16, p->n))
+                         : (dbg == 1 ? go(k_select_pack2<1, 4, uint16_t>, s16, p->n) : go(k_select_pack2<2, 4, uint16_t>, s16, p->n));
+      else
+#endif
+      if (idx16)
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t>, s16, p->n);
+      else
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t>, si, 0) : go(k_select_pack2<0, 4, int32_t>, si, 0);
+      if (rc2) return rc2;
     } else {
       // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory
       HINM_CUDA_TRY(smem_optin((const void*)k_select_pack<256, 4>, (int)fsmem));
