@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(NT) k_scores4(const uint16_t* __restrict__ W, 
 }
 
 // a3 (bf16 fast path, n % 8 == 0): 8 consecutive columns per thread (one 16-byte load per row, a
-// warp reads 512 contiguous bytes of a row), 8 rows of loads in flight (128 B per thread), still
+// warp reads 512 contiguous bytes of a row), RB rows of loads in flight (RB x 16 B per thread), still
 // summed sequentially in sigma_o row order per column.
-template <int NT>
+template <int NT, int RB = 8>
 __global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, int64_t ldw,
                                                 const int32_t* __restrict__ sigma_o, int n, int V,
                                                 double* __restrict__ scores, BselInit init) {
@@ -151,13 +151,13 @@ __global__ void __launch_bounds__(NT) k_scores8(const uint16_t* __restrict__ W, 
     }
   };
   int r = 0;
-  for (; r + 8 <= V; r += 8) {
-    uint4 v[8];
+  for (; r + RB <= V; r += RB) {  // RB rows of loads in flight per thread (RB x 16 B)
+    uint4 v[RB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < RB; ++u)
       v[u] = __ldcs(reinterpret_cast<const uint4*>(Wc + (int64_t)s_rows8[r + u] * ldw));
 #pragma unroll
-    for (int u = 0; u < 8; ++u) add(v[u], r + u == 0);
+    for (int u = 0; u < RB; ++u) add(v[u], r + u == 0);
   }
   for (; r < V; ++r) add(__ldcs(reinterpret_cast<const uint4*>(Wc + (int64_t)s_rows8[r] * ldw)), r == 0);
   double2* out = reinterpret_cast<double2*>(scores + (int64_t)t * n + j0);
@@ -1877,7 +1877,11 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   unsigned long long* keybits = (unsigned long long*)(ghist + BSEL_BINS + 4 + 2 * BSEL_CAP);
   const BselInit init{ghist, keybits};  // zeroed by the score kernel's first CTA
   if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
-    HINM_CUDA_TRY(launch_chain(k_scores8<128>, dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream,
+    auto ks = k_scores8<128, 8>;  // 16 / 32 rows in flight measured no faster (scripts/r03_gpu60.sh)
+#ifdef HINM_EXPERIMENTS
+    if (const char* e = getenv("HINM_SCORES_RB")) ks = atoi(e) == 8 ? k_scores8<128, 8> : atoi(e) == 32 ? k_scores8<128, 32> : ks;
+#endif
+    HINM_CUDA_TRY(launch_chain(ks, dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream,
                                W, ldw, sigma_o, n, V, scores, init));
   } else if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
     HINM_CUDA_TRY(launch_chain(k_scores4<128>, dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream,
