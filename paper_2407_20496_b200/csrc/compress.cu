@@ -7,7 +7,8 @@
 //   k_tile_sort (cub for n > 16384)   a4  per-tile stable descending sort of the scores (ties ->
 //                      lower column), only over the key bits that differ inside the tile
 //   k_gains        a4  gains[t,q] = numpy-pairwise sum of M sorted scores (+ key OR / AND)
-//   k_bsel_hist / _collect / _final, k_budget_radix   a5  global greedy == G smallest keys (-gain, q, t)
+//   k_bsel_hist / _collect (+ pick) / _bounds (+ tie order), k_budget_radix   a5  global greedy == G
+//                  smallest keys (-gain, q, t)
 //   k_tile_rank    a4  per-tile bitonic sort (score desc, column asc) + gains + sorted order
 //   k_survivors(_ord)   a6/a7 ascending survivors per tile, vector mask
 //   k_validate_sigma / k_dead_check   a7/a9 invariant checks (pruning.py:196-204, 226-254)
@@ -606,7 +607,7 @@ __device__ void budget_tail(const double* __restrict__ gains, int T, int G, int6
       lo_scr[t] = row_bound(row, G, xs, false);
       hi_scr[t] = row_bound(row, G, xs, true);
     }
-    const int l = lo_scr[t], h = hi_scr[t];
+    const int l = __ldcg(lo_scr + t), h = __ldcg(hi_scr + t);
     less += l;
     if (h > l) {
       qmin = min(qmin, (int64_t)l);
@@ -636,7 +637,7 @@ __device__ void budget_tail(const double* __restrict__ gains, int T, int G, int6
     int mid = (qlo + qhi) >> 1;
     int64_t f = 0;
     for (int t = threadIdx.x; t < T; t += NT) {
-      int v = min(hi_scr[t], mid + 1) - lo_scr[t];
+      int v = min(__ldcg(hi_scr + t), mid + 1) - __ldcg(lo_scr + t);
       f += v > 0 ? v : 0;
     }
     f = block_sum64<NT>(f, &red);
@@ -645,7 +646,7 @@ __device__ void budget_tail(const double* __restrict__ gains, int T, int G, int6
   const int Q = qlo;
   int64_t below = 0;
   for (int t = threadIdx.x; t < T; t += NT) {
-    int v = min(hi_scr[t], Q) - lo_scr[t];
+    int v = min(__ldcg(hi_scr + t), Q) - __ldcg(lo_scr + t);
     below += v > 0 ? v : 0;
   }
   below = block_sum64<NT>(below, &red);
@@ -659,7 +660,7 @@ __device__ void budget_tail(const double* __restrict__ gains, int T, int G, int6
     int t = base + threadIdx.x;
     int64_t at_q = 0, cnt = 0;
     if (t < T) {
-      int l = lo_scr[t], h = hi_scr[t];
+      int l = __ldcg(lo_scr + t), h = __ldcg(hi_scr + t);
       int v = min(h, Q) - l;
       cnt = l + (v > 0 ? v : 0);
       at_q = (l <= Q && Q < h) ? 1 : 0;
@@ -750,11 +751,12 @@ __global__ void __launch_bounds__(NT) k_budget_radix(const double* __restrict__ 
 }
 
 
-// a5, three plain launches (no grid barrier): (1) a 4096-bin histogram of the top 12 differing
-// bits of every budget key, (2) every CTA finds the bin holding rank G (redundantly, from the
-// 16 KB histogram) and appends the keys of that bin to a candidate list, (3) one CTA selects the
-// exact key among the candidates (block radix sort when they fit, else radix select over the
-// list), finds every tile's bounds around it and applies the (q, t) tie order (budget_tail).
+// a5, three plain launches (no grid barrier): (1) a 4096-bin histogram of the 12 bits below the
+// keys' common prefix, (2) every CTA finds the bin holding rank G (redundantly, from the 16 KB
+// histogram) and appends the keys of that bin to a candidate list; the last CTA to finish selects
+// the exact key among the candidates (bitonic sort when they fit, else radix select over the
+// bin's prefix), (3) one warp per tile finds the tile's bounds around it and the last CTA applies
+// the (q, t) tie order (budget_tail).
 constexpr int BSEL_BITS = 12, BSEL_BINS = 1 << BSEL_BITS, BSEL_CAP = 4096;
 static_assert(BselInit::kBselWords == BSEL_BINS + 4, "BselInit zeroes the histogram and the candidate count");
 
@@ -821,12 +823,31 @@ __device__ void bsel_find(const uint32_t* __restrict__ ghist, int64_t k, int* s_
   __syncthreads();
 }
 
+// "Last CTA done": true in the one CTA that finishes last, after every CTA's global writes are
+// visible to it (fence before the counter, fence after).  The counter is zeroed per call (BselInit).
+__device__ __forceinline__ bool last_cta(unsigned int* done) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
 template <int NT>
-__global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ gains, int64_t total,
+__device__ void bsel_pick(const double* __restrict__ gains, int T, int G, int64_t total_groups,
+                          const unsigned long long* __restrict__ keybits, const uint32_t* __restrict__ ghist,
+                          const unsigned long long* __restrict__ cand, const unsigned int* __restrict__ ncand,
+                          unsigned long long* __restrict__ xsel);
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ gains, int64_t total, int T, int G,
                                                      int64_t rank, const unsigned long long* __restrict__ keybits,
                                                      const uint32_t* __restrict__ ghist,
                                                      unsigned long long* __restrict__ cand,
-                                                     unsigned int* __restrict__ ncand) {
+                                                     unsigned int* __restrict__ ncand, unsigned int* __restrict__ done,
+                                                     unsigned long long* __restrict__ xsel) {
   pdl_enter();
   __shared__ int s_bin;
   __shared__ int64_t s_k;
@@ -846,20 +867,18 @@ __global__ void __launch_bounds__(NT) k_bsel_collect(const double* __restrict__ 
     const unsigned int slot = base + __popc(m & ((1u << lane) - 1u));
     if (in && slot < BSEL_CAP) cand[slot] = d;
   }
+  // the last CTA to finish picks the threshold key (bsel_pick below), saving a dependent launch
+  if (last_cta(done)) bsel_pick<NT>(gains, T, G, rank, keybits, ghist, cand, ncand, xsel);
 }
 
 // The threshold key x = the total_groups-th smallest budget key (one CTA): the rank's bin from the
 // global histogram, then the bitonic-sorted candidates of that bin (or, when a tie-heavy bin holds
 // more keys than the candidate list, an exact 8-bit radix select restricted to the bin's prefix).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_bsel_pick(const double* __restrict__ gains, int T, int G,
-                                                  int64_t total_groups,
-                                                  const unsigned long long* __restrict__ keybits,
-                                                  const uint32_t* __restrict__ ghist,
-                                                  const unsigned long long* __restrict__ cand,
-                                                  const unsigned int* __restrict__ ncand,
-                                                  unsigned long long* __restrict__ xsel) {
-  pdl_enter();
+__device__ void bsel_pick(const double* __restrict__ gains, int T, int G, int64_t total_groups,
+                          const unsigned long long* __restrict__ keybits, const uint32_t* __restrict__ ghist,
+                          const unsigned long long* __restrict__ cand, const unsigned int* __restrict__ ncand,
+                          unsigned long long* __restrict__ xsel) {
   __shared__ uint64_t s_cand[BSEL_CAP];
   __shared__ uint64_t s_x;
   __shared__ int s_bin;
@@ -918,34 +937,29 @@ __global__ void __launch_bounds__(NT) k_bsel_pick(const double* __restrict__ gai
 
 // Per-tile bounds around x, one warp per tile (all tiles in parallel: the 32-ary searches are
 // latency-bound, a single CTA walking ~10 tiles per warp took ~20 us on the LLaMA shapes).
+// ... and the last CTA applies the (q, t) tie order and writes tile_ptr (budget_tail).
 __global__ void __launch_bounds__(256) k_bsel_bounds(const double* __restrict__ gains, int T, int G,
+                                                     int64_t total_groups, int M,
                                                      const unsigned long long* __restrict__ xsel,
-                                                     int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr) {
+                                                     int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
+                                                     unsigned int* __restrict__ done, int32_t* __restrict__ tile_ptr) {
   pdl_enter();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (t >= T) return;
   const uint64_t x = __ldcg(xsel);
-  const double* row = gains + (int64_t)t * G;
-  const int a = row_bound_warp(row, G, x, false);
-  // ties of x inside a tile are rare: scan up from the lower bound before the full search
-  int b = a;
-  const int p = a + lane;
-  const bool eq = p < G && gain_key(row[p]) == x;
-  const uint32_t m = __ballot_sync(0xffffffffu, !eq);
-  b = m ? a + __ffs(m) - 1 : row_bound_warp(row, G, x, true);
-  if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
+  if (t < T) {
+    const double* row = gains + (int64_t)t * G;
+    const int a = row_bound_warp(row, G, x, false);
+    // ties of x inside a tile are rare: scan up from the lower bound before the full search
+    int b = a;
+    const int p = a + lane;
+    const bool eq = p < G && gain_key(row[p]) == x;
+    const uint32_t m = __ballot_sync(0xffffffffu, !eq);
+    b = m ? a + __ffs(m) - 1 : row_bound_warp(row, G, x, true);
+    if (lane == 0) { lo_scr[t] = a; hi_scr[t] = b; }
+  }
+  if (last_cta(done)) budget_tail<256>(gains, T, G, total_groups, M, x, false, lo_scr, hi_scr, tile_ptr);
 }
 
-// Per-tile counts with the (q, t) tie order, written as the tile_ptr prefix (one CTA).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_bsel_tail(const double* __restrict__ gains, int T, int G,
-                                                  int64_t total_groups, int M,
-                                                  const unsigned long long* __restrict__ xsel,
-                                                  int32_t* __restrict__ lo_scr, int32_t* __restrict__ hi_scr,
-                                                  int32_t* __restrict__ tile_ptr) {
-  pdl_enter();
-  budget_tail<NT>(gains, T, G, total_groups, M, __ldcg(xsel), false, lo_scr, hi_scr, tile_ptr);
-}
 
 // a6/a7: survivors of tile t = order[t][0:k_t]; emitted in ascending column order.
 template <int NT>
@@ -1940,14 +1954,11 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
       unsigned long long* xsel = keybits + 2;
       const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms / 4, ceil_div(total, 4096)));
       HINM_CUDA_TRY(launch_chain(k_bsel_hist<1024>, nblk, 1024, 0, stream, gains, total, keybits, ghist));
-      HINM_CUDA_TRY(launch_chain(k_bsel_collect<1024>, nblk, 1024, 0, stream, gains, total, groups, keybits, ghist,
-                                 cand, ncand));
-      HINM_CUDA_TRY(launch_chain(k_bsel_pick<512>, 1, 512, 0, stream, gains, T, G, groups, keybits, ghist, cand,
-                                 ncand, xsel));
-      HINM_CUDA_TRY(launch_chain(k_bsel_bounds, (unsigned)ceil_div(T, 8), 256, 0, stream, gains, T, G, xsel, lo_s,
-                                 hi_s));
-      HINM_CUDA_TRY(launch_chain(k_bsel_tail<512>, 1, 512, 0, stream, gains, T, G, groups, M, xsel, lo_s, hi_s,
-                                 tile_ptr));
+      unsigned int* done = ncand + 1;  // two "last CTA" counters, zeroed with the histogram
+      HINM_CUDA_TRY(launch_chain(k_bsel_collect<1024>, nblk, 1024, 0, stream, gains, total, T, G, groups, keybits,
+                                 ghist, cand, ncand, done, xsel));
+      HINM_CUDA_TRY(launch_chain(k_bsel_bounds, (unsigned)ceil_div(T, 8), 256, 0, stream, gains, T, G, groups, M,
+                                 xsel, lo_s, hi_s, done + 1, tile_ptr));
     }
   }
   if (fused) {
