@@ -19,6 +19,7 @@
 //               vectors): nm_index / kept_values per (row, chunk), then hinm_pack_build writes the
 //               tcgen05 operand image exactly as for a V = 128 pack
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -81,6 +82,175 @@ __global__ void k_masks(const int32_t* __restrict__ tile_ptr, const int32_t* __r
   }
 }
 
+// First-fit chunking of one group's union columns (one CTA per group).  Open chunks form a list
+// in creation order; a column c with row set m fits entry e iff twos[e] & m == 0 (rows with >= 2
+// nonzeros in the chunk) and the chunk has a free slot; it joins the lowest fitting entry, else a
+// new chunk is appended.  The list state lives in registers: thread tid owns entries
+// 4 tid .. 4 tid + 3 (ones / twos masks of all 256 rows, fill count, chunk id), so a column costs
+// one broadcast of its mask, 64 register ANDs per thread, a warp min and one barrier (the owner
+// updates its entry).  Full chunks stay in the list until it reaches EMAX entries, then a stable
+// compaction through shared memory drops them; if the open chunks alone fill the list the oldest
+// is closed (deterministic).  Output: chunk_cols[u][4 * chunk + slot] (column, -1 = empty slot),
+// nchunks[u].
+__global__ void __launch_bounds__(GT, 1) k_greedy(const uint32_t* __restrict__ mask, int n, int cap_chunks,
+                                                  int32_t* __restrict__ chunk_cols, int32_t* __restrict__ nchunks) {
+  constexpr int PER = EMAX / GT;
+  extern __shared__ __align__(16) uint32_t gsm[];
+  uint32_t* st_ones = gsm;                                   // compaction staging [EMAX][MW]
+  uint32_t* st_twos = st_ones + EMAX * MW;
+  int32_t* st_cid = reinterpret_cast<int32_t*>(st_twos + EMAX * MW);
+  int32_t* st_cnt = st_cid + EMAX;
+  __shared__ uint32_t bm[GT][MW + 1];
+  __shared__ int bcol[GT];
+  __shared__ int s_wsum[GT / 32], s_wmin[2][GT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = blockIdx.x;
+  const uint32_t* mu = mask + (int64_t)u * n * MW;
+  int32_t* cc = chunk_cols + (int64_t)u * cap_chunks * 4;
+  uint32_t on[PER][MW], tw[PER][MW];
+  int cn[PER], id[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    cn[q] = 4;
+    id[q] = 0;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) on[q][w] = tw[q][w] = 0u;
+  }
+  int L = 0, nchunk = 0, it = 0;  // list length and chunk count: identical in every thread
+  for (int c0 = 0; c0 < n; c0 += GT) {
+    // ---- batch of GT columns: keep the ones some row of the group uses (the union), in order
+    const int c = c0 + tid;
+    uint32_t m[MW];
+    bool nz = false;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+      m[w] = c < n ? mu[(int64_t)c * MW + w] : 0u;
+      nz |= m[w] != 0u;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) s_wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, nb = 0;
+    for (int w = 0; w < GT / 32; ++w) {
+      off += w < warp ? s_wsum[w] : 0;
+      nb += s_wsum[w];
+    }
+    if (nz) {
+      const int pos = off + __popc(bal & ((1u << lane) - 1u));
+#pragma unroll
+      for (int w = 0; w < MW; ++w) bm[pos][w] = m[w];
+      bcol[pos] = c;
+    }
+    __syncthreads();
+    for (int i = 0; i < nb; ++i, ++it) {
+      uint32_t mm[MW];
+#pragma unroll
+      for (int w = 0; w < MW; ++w) mm[w] = bm[i][w];
+      int mine = INT_MAX;
+#pragma unroll
+      for (int q = PER - 1; q >= 0; --q) {  // the thread's lowest fitting entry
+        uint32_t conf = 0u;
+#pragma unroll
+        for (int w = 0; w < MW; ++w) conf |= tw[q][w] & mm[w];
+        if (tid * PER + q < L && cn[q] < 4 && conf == 0u) mine = tid * PER + q;
+      }
+      mine = __reduce_min_sync(0xffffffffu, mine);
+      // double-buffered warp minima: the buffer written at column it + 2 is behind column it + 1's barrier
+      if (lane == 0) s_wmin[it & 1][warp] = mine;
+      __syncthreads();
+      int bj = INT_MAX;
+#pragma unroll
+      for (int w = 0; w < GT / 32; ++w) bj = min(bj, s_wmin[it & 1][w]);
+      const int tgt = bj != INT_MAX ? bj : L;  // the entry that takes the column
+      if (tid == tgt / PER) {
+        // the owner updates entry qs with selects over its four entries (a branch on qs would let
+        // the compiler index the register arrays dynamically, i.e. move them to local memory)
+        const int qs = tgt % PER;
+        const bool grow = bj != INT_MAX;
+        int idq = 0, cnq = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          idq = q == qs ? id[q] : idq;
+          cnq = q == qs ? cn[q] : cnq;
+        }
+        if (grow) cc[(int64_t)idq * 4 + cnq] = bcol[i];
+        else *reinterpret_cast<int4*>(cc + (int64_t)nchunk * 4) = make_int4(bcol[i], -1, -1, -1);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const bool hit = q == qs;
+#pragma unroll
+          for (int w = 0; w < MW; ++w) {
+            const uint32_t t2 = grow ? (tw[q][w] | (on[q][w] & mm[w])) : 0u;
+            const uint32_t o2 = grow ? (on[q][w] | mm[w]) : mm[w];
+            tw[q][w] = hit ? t2 : tw[q][w];
+            on[q][w] = hit ? o2 : on[q][w];
+          }
+          cn[q] = hit ? (grow ? cn[q] + 1 : 1) : cn[q];
+          id[q] = hit && !grow ? nchunk : id[q];
+        }
+      }
+      if (bj == INT_MAX) {
+        ++L;
+        ++nchunk;
+      }
+      while (L == EMAX) {
+        // ---- stable compaction of the open entries through shared memory; if the open chunks
+        // alone fill the list, the oldest is closed and the loop compacts again
+        int open = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) open += cn[q] < 4;
+        int incl = open;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        int base = incl - open, tot = 0;
+        for (int w = 0; w < GT / 32; ++w) {
+          base += w < warp ? s_wsum[w] : 0;
+          tot += s_wsum[w];
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          if (cn[q] < 4) {
+#pragma unroll
+            for (int w = 0; w < MW; ++w) {
+              st_ones[base * MW + w] = on[q][w];
+              st_twos[base * MW + w] = tw[q][w];
+            }
+            st_cid[base] = id[q];
+            st_cnt[base] = cn[q];
+            ++base;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const int e = tid * PER + q;
+          if (e < tot) {
+#pragma unroll
+            for (int w = 0; w < MW; ++w) {
+              on[q][w] = st_ones[e * MW + w];
+              tw[q][w] = st_twos[e * MW + w];
+            }
+            id[q] = st_cid[e];
+            cn[q] = (tot == EMAX && e == 0) ? 4 : st_cnt[e];
+          } else {
+            cn[q] = 4;
+          }
+        }
+        L = tot;
+        __syncthreads();  // staging and s_wsum are reused by the next compaction / batch
+      }
+    }
+    __syncthreads();  // bm / bcol are refilled by the next batch
+  }
+  if (tid == 0) nchunks[u] = nchunk;
+}
+
+#ifdef HINM_EXPERIMENTS
 // First-fit chunking of one group's union columns (one CTA per group).  Open chunks live in a
 // list in creation order (SoA: ones / twos = rows with >= 1 / >= 2 nonzeros in the chunk); a column
 // c with row set m fits chunk e iff twos[e] & m == 0.  Each thread scans its entries e = tid +
@@ -88,7 +258,7 @@ __global__ void k_masks(const int32_t* __restrict__ tile_ptr, const int32_t* __r
 // chunks stay in the list (skipped) until the list reaches EMAX, then a stable compaction drops
 // them; if the live open chunks alone fill the list the oldest open one is closed (deterministic).
 // Output: chunk_cols[u][4 * chunk + slot] (column, -1 = empty slot), nchunks[u].
-__global__ void __launch_bounds__(GT, 1) k_greedy(const uint32_t* __restrict__ mask, int n, int cap_chunks,
+__global__ void __launch_bounds__(GT, 1) k_greedy_smem(const uint32_t* __restrict__ mask, int n, int cap_chunks,
                                                   int32_t* __restrict__ chunk_cols, int32_t* __restrict__ nchunks) {
   extern __shared__ __align__(16) uint32_t gsm[];
   uint32_t* ones = gsm;                                    // [MW][EMAX]
@@ -249,6 +419,8 @@ __global__ void __launch_bounds__(GT, 1) k_greedy(const uint32_t* __restrict__ m
   if (tid == 0) nchunks[u] = s_nchunk;
 }
 
+#endif
+
 // Pseudo-tile offsets: pseudo tile 2u + h has 4 * nchunks[u] vectors.
 __global__ void k_gptr(const int32_t* __restrict__ nchunks, int U, int32_t* __restrict__ gptr) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -371,9 +543,17 @@ extern "C" int hinm_group_plan(const hinm_pack_t* p, void* ws, size_t ws_bytes, 
   const int mgx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n / 4, 8 / (V / 32)), 64));
   k_masks<<<dim3(mgx, T), 256, 0, stream>>>(p->tile_ptr, p->vec_idx, p->nm_pos, n, V, mask);
   HINM_LAUNCH_CHECK();
-  const size_t gsmem = (size_t)4 * MW * EMAX * 4 + (size_t)4 * EMAX * 4;
-  HINM_CUDA_TRY(smem_optin((const void*)k_greedy, (int)gsmem));
-  k_greedy<<<U, GT, gsmem, stream>>>(mask, n, n, cols, nch);
+  const size_t gsmem = (size_t)2 * MW * EMAX * 4 + (size_t)2 * EMAX * 4;  // compaction staging
+  auto kg = k_greedy;
+  size_t ksmem = gsmem;
+#ifdef HINM_EXPERIMENTS
+  if (getenv("HINM_GREEDY_SMEM")) {  // the shared-memory list (A / B of identical chunking)
+    kg = k_greedy_smem;
+    ksmem = (size_t)4 * MW * EMAX * 4 + (size_t)4 * EMAX * 4;
+  }
+#endif
+  HINM_CUDA_TRY(smem_optin((const void*)kg, (int)ksmem));
+  kg<<<U, GT, ksmem, stream>>>(mask, n, n, cols, nch);
   HINM_LAUNCH_CHECK();
   HINM_CUDA_TRY(cudaMemcpyAsync(nchunks_host, nch, (size_t)U * 4, cudaMemcpyDeviceToHost, stream));
   HINM_CUDA_TRY(cudaStreamSynchronize(stream));
