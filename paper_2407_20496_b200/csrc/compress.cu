@@ -554,6 +554,38 @@ __global__ void __launch_bounds__(NT, rank_min_blocks<NT>()) k_tile_rank(
   }
 }
 
+// Operand-image offsets of every tile (one CTA): kofs[t] = sum of round_up(k_t', 64) over t' < t,
+// eofs[t] = the same in 128-K metadata blocks.
+template <int NT>
+__device__ void pack_offsets_body(const int32_t* __restrict__ tile_ptr, int T, int32_t* __restrict__ kofs,
+                                  int32_t* __restrict__ eofs) {
+  typedef cub::BlockScan<int, NT> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int carry_k, carry_e;
+  if (threadIdx.x == 0) { carry_k = 0; carry_e = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += NT) {
+    const int t = base + threadIdx.x;
+    int kp = 0, eb = 0;
+    if (t < T) {
+      kp = (int)round_up(tile_ptr[t + 1] - tile_ptr[t], 64);
+      eb = (int)ceil_div(kp, 128);
+    }
+    int ek, ee, tk, te;
+    BS(tmp).ExclusiveSum(kp, ek, tk);
+    __syncthreads();
+    BS(tmp).ExclusiveSum(eb, ee, te);
+    if (t < T) {
+      kofs[t] = carry_k + ek;
+      eofs[t] = carry_e + ee;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { carry_k += tk; carry_e += te; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { kofs[T] = carry_k; eofs[T] = carry_e; }
+}
+
 // a6/a7: survivors of tile t = its first k_t sorted columns, emitted in ascending column order
 // (the default sigma_i, pruning.py:167-169) with the vector mask row: flag the k_t columns, then
 // one block scan over contiguous per-thread column ranges.
@@ -561,7 +593,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict__ order16, int n,
                                                       const int32_t* __restrict__ tile_ptr,
                                                       int32_t* __restrict__ surv, uint8_t* __restrict__ vmask,
-                                                      uint16_t* __restrict__ surv16) {
+                                                      uint16_t* __restrict__ surv16, int32_t* __restrict__ kofs,
+                                                      int32_t* __restrict__ eofs) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t sv_flags[];
   typedef cub::BlockScan<int, NT> BS;
@@ -590,6 +623,8 @@ __global__ void __launch_bounds__(NT) k_survivors_ord(const uint16_t* __restrict
     uint8_t* vm = vmask + (int64_t)t * n;
     for (int j = threadIdx.x; j < n; j += NT) vm[j] = sv_flags[j];
   }
+  // the operand image's tile offsets (compress path: one launch fewer before select + pack)
+  if (kofs && blockIdx.x == 0) pack_offsets_body<NT>(tile_ptr, gridDim.x, kofs, eofs);
 }
 
 // Tail of the budget selection once the threshold key xs (the G-th smallest (-gain) key) is
@@ -1235,31 +1270,7 @@ __global__ void __launch_bounds__(NT) k_pack_offsets(const int32_t* __restrict__
                                                      int32_t* __restrict__ kofs,
                                                      int32_t* __restrict__ eofs) {
   pdl_enter();
-  typedef cub::BlockScan<int, NT> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ int carry_k, carry_e;
-  if (threadIdx.x == 0) { carry_k = 0; carry_e = 0; }
-  __syncthreads();
-  for (int base = 0; base < T; base += NT) {
-    const int t = base + threadIdx.x;
-    int kp = 0, eb = 0;
-    if (t < T) {
-      kp = (int)round_up(tile_ptr[t + 1] - tile_ptr[t], 64);
-      eb = (int)ceil_div(kp, 128);
-    }
-    int ek, ee, tk, te;
-    BS(tmp).ExclusiveSum(kp, ek, tk);
-    __syncthreads();
-    BS(tmp).ExclusiveSum(eb, ee, te);
-    if (t < T) {
-      kofs[t] = carry_k + ek;
-      eofs[t] = carry_e + ee;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { carry_k += tk; carry_e += te; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { kofs[T] = carry_k; eofs[T] = carry_e; }
+  pack_offsets_body<NT>(tile_ptr, T, kofs, eofs);
 }
 
 __device__ __forceinline__ int64_t aval_offset(int64_t kofs_t, int V, int r, int kc) {
@@ -1530,15 +1541,10 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     uint8_t* __restrict__ nm_pos, uint16_t* __restrict__ kept, uint16_t* __restrict__ a_vals,
     uint32_t* __restrict__ a_meta, int32_t* __restrict__ gidx) {
   static_assert(NS % 4 == 0 && NS <= 16, "the ring holds whole quads of rows");
-  pdl_enter();
   constexpr int NC = 32 * SP2_CWARPS;
   extern __shared__ __align__(128) uint8_t sp2_smem[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS], idx_bar;
   const int t = blockIdx.y, r0 = blockIdx.x * SP2_ROWS;
-  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
-  const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
-  const int eofs = eofs_g[t], nblk = eofs_g[t + 1] - eofs;
-  if (kp == 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)n * 2;  // host: n % 8 == 0
   uint8_t* s_rows = sp2_smem;
@@ -1557,29 +1563,50 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
   }
   __syncthreads();
   const int nrows = min(SP2_ROWS, V - r0);
+  const bool producer = warp == SP2_CWARPS && lane == 0;
+  auto bulk = [&](uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  // The weight rows need nothing from the chain before this kernel (W was complete before its first
+  // kernel started, sigma_o is an input): the producer starts the first NS rows before waiting for
+  // the previous grid, so they stream in during the predecessor's tail.
+  int32_t rows[SP2_ROWS];
+  if (producer) {
+#pragma unroll
+    for (int i = 0; i < SP2_ROWS; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
+#pragma unroll
+    for (int rr = 0; rr < NS; ++rr) {
+      if (rr >= nrows) break;
+      if (DBG == 2)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * rr) : "memory");
+      else
+        bulk(rows_u32 + rr * row_bytes, W + (int64_t)rows[rr] * ldw, row_bytes, full0 + 8 * rr);
+    }
+  }
+  pdl_enter();  // survivors / tile offsets / outputs: after the previous grid
+  const int b = sig_ptr[t], k = sig_ptr[t + 1] - b, G = k / 4;
+  const int kofs = kofs_g[t], kp = kofs_g[t + 1] - kofs;
+  const int eofs = eofs_g[t], nblk = eofs_g[t + 1] - eofs;
+  if (kp == 0) {  // empty tile: drain the rows already in flight, then exit
+    if (producer)
+      for (int rr = 0; rr < NS && rr < nrows; ++rr) sp_mbar_wait(full0 + 8 * rr, 0);
+    return;
+  }
   if (warp == SP2_CWARPS) {
     // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      auto bulk = [&](uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                     "l"(src), "r"(bytes), "r"(bar)
-                     : "memory");
-      };
+    if (producer) {
       // k % 4 == 0; a uint16 list is read to the next 16 bytes (inside the tile's n-stride slot)
       const IDX* src = sig_idx + (idx_stride ? (int64_t)t * idx_stride : (int64_t)b);
       bulk((uint32_t)__cvta_generic_to_shared(s_idx), src, ((uint32_t)k * (uint32_t)sizeof(IDX) + 15u) & ~15u, ibar);
-      int32_t rows[SP2_ROWS];
 #pragma unroll
-      for (int i = 0; i < SP2_ROWS; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
-#pragma unroll
-      for (int rr = 0; rr < SP2_ROWS; ++rr) {
+      for (int rr = NS; rr < SP2_ROWS; ++rr) {
         if (rr >= nrows) break;
         const int slot = rr % NS, use = rr / NS;
-        if (use > 0) {
-          sp_mbar_wait(empty0 + 8 * slot, (use - 1) & 1);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
-        }
+        sp_mbar_wait(empty0 + 8 * slot, (use - 1) & 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
         if (DBG == 2)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * slot) : "memory");
         else
@@ -1862,11 +1889,12 @@ extern "C" int hinm_pack_capacity(int m, int n, int V, int64_t total_keep, int64
   return HINM_OK;
 }
 
-extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd,
-                                 const double* S, int64_t lds, const int32_t* sigma_o, int m,
-                                 int n, int V, int M, int64_t total_keep, int32_t* tile_ptr,
-                                 int32_t* surv, uint8_t* vector_mask, void* workspace,
-                                 size_t workspace_bytes, void* stream_) {
+// hinm_vector_prune, optionally also writing the operand image's tile offsets (kofs / eofs, non-NULL:
+// only on the fused path, prune_fused(n, M))
+static int vector_prune_impl(const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd, const double* S,
+                             int64_t lds, const int32_t* sigma_o, int m, int n, int V, int M, int64_t total_keep,
+                             int32_t* tile_ptr, int32_t* surv, uint8_t* vector_mask, void* workspace,
+                             size_t workspace_bytes, void* stream_, int32_t* kofs, int32_t* eofs) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!W && !Wd && !S) return HINM_ERR_VALUE;
   WsLayout L;
@@ -1965,7 +1993,7 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
     const size_t fsm = (size_t)round_up(n, 16);
     HINM_CUDA_TRY(smem_optin((const void*)k_survivors_ord<512>, (int)fsm + 4096));
     HINM_CUDA_TRY(launch_chain(k_survivors_ord<512>, T, 512, fsm, stream, order16, n, tile_ptr, surv, vector_mask,
-                               (uint16_t*)(ws + L.surv16)));
+                               (uint16_t*)(ws + L.surv16), kofs, eofs));
     return HINM_OK;
   }
   const size_t smem = (size_t)n;
@@ -1974,6 +2002,15 @@ extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* W
   k_survivors<1024><<<T, 1024, smem, stream>>>(order, n, tile_ptr, surv, vector_mask);
   HINM_LAUNCH_CHECK();
   return HINM_OK;
+}
+
+extern "C" int hinm_vector_prune(const uint16_t* W, int64_t ldw, const double* Wd, int64_t ldwd,
+                                 const double* S, int64_t lds, const int32_t* sigma_o, int m,
+                                 int n, int V, int M, int64_t total_keep, int32_t* tile_ptr,
+                                 int32_t* surv, uint8_t* vector_mask, void* workspace,
+                                 size_t workspace_bytes, void* stream_) {
+  return vector_prune_impl(W, ldw, Wd, ldwd, S, lds, sigma_o, m, n, V, M, total_keep, tile_ptr, surv, vector_mask,
+                           workspace, workspace_bytes, stream_, nullptr, nullptr);
 }
 
 extern "C" int hinm_nm_select(int mode, const uint16_t* W, int64_t ldw, const double* Wd,
@@ -2095,8 +2132,12 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
   const bool own_sigma = sig_idx == nullptr;
   int32_t* surv = own_sigma ? p->vec_idx : (int32_t*)((char*)workspace + L.surv_tmp);
   int32_t* tptr = p->tile_ptr;
-  st = hinm_vector_prune(W, ldw, nullptr, 0, S, lds, sigma_o, p->m, p->n, p->V, p->M,
-                         p->total_keep, tptr, surv, vmask, workspace, workspace_bytes, stream_);
+  // own sigma_i on the fused prune path: the survivors kernel also writes the operand image's tile
+  // offsets (the select + pack below then follows it directly)
+  const bool offs_early = own_sigma && prune_fused(p->n, p->M) && p->tile_kofs && p->tile_eofs;
+  st = vector_prune_impl(W, ldw, nullptr, 0, S, lds, sigma_o, p->m, p->n, p->V, p->M, p->total_keep, tptr, surv,
+                         vmask, workspace, workspace_bytes, stream_, offs_early ? p->tile_kofs : nullptr,
+                         offs_early ? p->tile_eofs : nullptr);
   if (st) return st;
   const int32_t* sp = own_sigma ? tptr : sig_ptr;
   const int32_t* si = own_sigma ? surv : sig_idx;
@@ -2120,8 +2161,9 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
     int64_t kcap = 0, mcap = 0, acap = 0;
     hinm_pack_capacity(p->m, p->n, p->V, p->total_keep, &kcap, &mcap, &acap);
     if (p->kpad_cap < kcap || p->meta_words_cap < mcap) return HINM_ERR_WORKSPACE;
-    HINM_CUDA_TRY(launch_chain(k_pack_offsets<256>, 1, 256, 0, stream, (const int32_t*)tptr, p->T, p->tile_kofs,
-                               p->tile_eofs));
+    if (!offs_early)
+      HINM_CUDA_TRY(launch_chain(k_pack_offsets<256>, 1, 256, 0, stream, (const int32_t*)tptr, p->T, p->tile_kofs,
+                                 p->tile_eofs));
     // streamed variant (k_select_pack2): rows bulk-copied through a ring, 16 rows per CTA; needs
     // 16-byte rows (n % 8 == 0) and a ring of >= 2 rows in ~100 KB (two CTAs per SM)
     const size_t rowb = (size_t)p->n * 2;

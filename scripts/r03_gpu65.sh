@@ -1,0 +1,7 @@
+#!/bin/bash
+# tile offsets from the survivors kernel + W rows streamed before griddepcontrol.wait in select + pack
+set -u
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_image.py tests/test_gpu_ties.py tests/test_gpu_bench_step.py tests/test_gpu_group.py tests/test_gpu_chain.py tests/test_gpu_next.py -x -q 2>&1 | tail -1
+for i in 1 2 3; do timeout 300 python scripts/compress_time.py 20 2>&1 | tail -1 | python3 -c "import json,sys; d=json.load(sys.stdin); print({k:(v['gpu_ms'],v['b2b_ms'],v['graph_matches_eager']) for k,v in d.items()})"; done
+timeout 900 compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py 2>&1 | tail -1
+timeout 900 compute-sanitizer --tool synccheck python scripts/sanitize_smoke.py 2>&1 | tail -1
