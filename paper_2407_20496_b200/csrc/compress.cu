@@ -1920,10 +1920,15 @@ static int vector_prune_impl(const uint16_t* W, int64_t ldw, const double* Wd, i
   const BselInit init{ghist, keybits};  // zeroed by the score kernel's first CTA
   if (W && !Wd && !S && n >= 2 && (n % 8) == 0 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0) {
     auto ks = k_scores8<128, 8>;  // 16 / 32 rows in flight measured no faster (scripts/r03_gpu60.sh)
+    int snt = 128;
 #ifdef HINM_EXPERIMENTS
     if (const char* e = getenv("HINM_SCORES_RB")) ks = atoi(e) == 8 ? k_scores8<128, 8> : atoi(e) == 32 ? k_scores8<128, 32> : ks;
+    if (const char* e = getenv("HINM_SCORES_NT")) {
+      snt = atoi(e) == 512 ? 512 : atoi(e) == 256 ? 256 : 128;
+      ks = snt == 512 ? k_scores8<512, 8> : snt == 256 ? k_scores8<256, 8> : ks;
+    }
 #endif
-    HINM_CUDA_TRY(launch_chain(ks, dim3((unsigned)ceil_div(n, 1024), T), 128, (size_t)V * 4, stream,
+    HINM_CUDA_TRY(launch_chain(ks, dim3((unsigned)ceil_div(n, 8 * snt), T), snt, (size_t)V * 4, stream,
                                W, ldw, sigma_o, n, V, scores, init));
   } else if (W && !Wd && !S && n >= 2 && (n % 4) == 0 && (ldw % 4) == 0 && ((uintptr_t)W & 7) == 0) {
     HINM_CUDA_TRY(launch_chain(k_scores4<128>, dim3((unsigned)ceil_div(n, 512), T), 128, (size_t)V * 4, stream,
