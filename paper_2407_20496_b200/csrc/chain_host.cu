@@ -138,7 +138,11 @@ extern "C" int hinm_chain_run_host(const hinm_chain_step_t* steps, int nsteps, c
     // compute: after the input arrived and the slot's previous result was copied out
     HINM_CUDA_TRY(cudaStreamWaitEvent(st, cs->h2d_done[slot], 0));
     if (c >= NSLOT) HINM_CUDA_TRY(cudaStreamWaitEvent(st, cs->d2h_done[slot], 0));
-    static const bool no_compute = getenv("HINM_CHAIN_NOCOMPUTE") != nullptr;  // diagnostics
+#ifdef HINM_EXPERIMENTS
+    static const bool no_compute = getenv("HINM_CHAIN_NOCOMPUTE") != nullptr;  // copy pipeline alone
+#else
+    constexpr bool no_compute = false;
+#endif
     for (int i = 0; i < nsteps && !no_compute; ++i) {
       const hinm_chain_step_t& s = steps[i];
       rc = hinm_spmm_bf16(s.pack, buf(slot, s.src), chunk_tokens, w, buf(slot, s.dst), chunk_tokens,
