@@ -121,3 +121,14 @@ def test_sass_has_cta_pair_mma():
     sass = subprocess.run([cuobjdump, "-sass", _lib_path()], capture_output=True, text=True).stdout
     for mnem in ("UTCHMMA.2CTA", "UTCBAR.2CTA.MULTICAST"):
         assert mnem in sass, mnem
+
+
+def test_product_library_has_only_validated_knobs():
+    """The product library reads only the documented tuning knobs (each validated: an unknown value
+    is an error, results are unchanged); the timing-only / diagnostic switches whose results are
+    garbage (HINM_PAIR_DBG, HINM_SP2, HINM_CHAIN_NOCOMPUTE, HINM_COMPRESS_PDL, ...) and the
+    timing-only kernel variants exist only in the experiments build."""
+    blob = open(_lib_path(), "rb").read()
+    knobs = sorted(set(re.findall(rb"HINM_[A-Z0-9_]+", blob)))
+    assert [k.decode() for k in knobs] == ["HINM_BN", "HINM_GATHER", "HINM_GROUPS", "HINM_GW", "HINM_KS",
+                                           "HINM_PAIR_GW", "HINM_PAIR_KS", "HINM_PDL", "HINM_Y_V8"]
