@@ -1081,11 +1081,13 @@ bool choose_group(const hinm_pack_t* pk, int B, int sms) {
   auto steps = [](double k) { return std::ceil(k / 64.0) * 2.0; };  // kp = round_up(k, 64) in 32-K steps
   const double st_t = steps((double)pk->total_keep / pk->T), st_g = steps((double)g->total_keep / g->T);
   const double waves_t = std::ceil(pk->T * nb / sms), waves_g = std::ceil(g->T / 2 * nb / (sms / 2));
-  const double floor_g = st_g <= 4.0 && B > 262144 ? 12000.0 : 5000.0;
-  const double cost_t = 3000.0 + waves_t * (st_t * 270.0 + 2300.0);
+  // constants fitted to minimise the time lost to wrong picks over 84 measured (shape, tokens)
+  // cases (scripts/fit_image_model.py on profiles/r02_image_choice_data.jsonl: 38.9 -> 16.9 us)
+  const double floor_g = st_g <= 4.0 && B > 262144 ? 11000.0 : 5000.0;
+  const double cost_t = 2000.0 + waves_t * (st_t * 270.0 + 2400.0);
   // short pair launches overlap their prologue with the previous kernel (PDL): a smaller ramp
   const double ramp_g = g->T / 2 * nb <= 8.0 * (sms / 2) ? 5000.0 : 8000.0;
-  const double cost_g = ramp_g + waves_g * std::max(st_g * 226.0 + 3300.0, floor_g);
+  const double cost_g = ramp_g + waves_g * std::max(st_g * 205.0 + 1900.0, floor_g);
   return cost_g < cost_t;
 }
 
