@@ -42,7 +42,7 @@ def timed(fn, graph, steps=20, warm=5):
     return s.elapsed_time(e) / steps * 1e3
 
 
-for cfg in sys.argv[1:]:
+for cfg in (sys.argv[1:] if __name__ == "__main__" else []):  # importable for timed()
     for i, (label, m, n, tokens, v, sv, count, graph) in enumerate(bench.cfg_cases(cfg)):
         g = torch.Generator(device=dev).manual_seed(31 + i)
         W = torch.randn(m, n, generator=g, device=dev).to(torch.bfloat16)
