@@ -162,6 +162,11 @@ int hinm_pack_build(hinm_pack_t* pack, void* stream);
  * vector_prune / nm_prune as in cli.py:189-190); the kept values always come from W.  `pack`
  * buffers are caller-allocated with the capacities above; sig_ptr/sig_idx NULL selects ascending
  * survivors.  Synchronizing only when a caller sigma_i is validated.
+ * The compressor's kernels (here and in hinm_vector_prune) are one dependent chain launched with
+ * programmatic stream serialization: each waits for its predecessor (griddepcontrol.wait) before
+ * touching memory, so ordinary stream order holds for the caller -- a plain launch after the call
+ * waits for all of it; a caller's own PDL-launched kernel must wait as usual before reading the
+ * outputs.  The call ends with hinm_stream_fence (see below).
  */
 int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* saliency, int64_t lds,
                        const int32_t* sigma_o, const int32_t* sig_ptr, const int32_t* sig_idx,
