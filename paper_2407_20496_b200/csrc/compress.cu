@@ -1514,7 +1514,6 @@ __device__ __forceinline__ void from_mask(uint32_t m, uint32_t w01, uint32_t w23
   nib = p0 | (p1 << 2);
 }
 
-constexpr int SP2_ROWS = 16;
 constexpr int SP2_CWARPS = 8;  // consumer warps; warp 8 is the producer
 
 // Producer warp 8: the tile's gather indices (one bulk copy of the k int32 column ids) and the 16
@@ -1533,7 +1532,9 @@ __device__ __forceinline__ int4 grp_idx(const uint16_t* s, int g) {
 }
 
 // sig_idx: tile t's ids at sig_idx + sig_ptr[t] (idx_stride == 0) or at sig_idx + t * idx_stride.
-template <int DBG = 0, int NS = 8, typename IDX = int32_t>
+// R = rows per CTA (16; 32 when a CTA's ring fills the SM: the per-CTA start-up is then paid once
+// per 32 rows instead of 16)
+template <int DBG = 0, int NS = 8, typename IDX = int32_t, int R = 16>
 __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
     const int32_t* __restrict__ sig_ptr, const IDX* __restrict__ sig_idx, int idx_stride, int n, int V,
@@ -1544,7 +1545,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
   constexpr int NC = 32 * SP2_CWARPS;
   extern __shared__ __align__(128) uint8_t sp2_smem[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS], idx_bar;
-  const int t = blockIdx.y, r0 = blockIdx.x * SP2_ROWS;
+  const int t = blockIdx.y, r0 = blockIdx.x * R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)n * 2;  // host: n % 8 == 0
   uint8_t* s_rows = sp2_smem;
@@ -1562,7 +1563,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int nrows = min(SP2_ROWS, V - r0);
+  const int nrows = min(R, V - r0);
   const bool producer = warp == SP2_CWARPS && lane == 0;
   auto bulk = [&](uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -1573,10 +1574,10 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
   // The weight rows need nothing from the chain before this kernel (W was complete before its first
   // kernel started, sigma_o is an input): the producer starts the first NS rows before waiting for
   // the previous grid, so they stream in during the predecessor's tail.
-  int32_t rows[SP2_ROWS];
+  int32_t rows[R];
   if (producer) {
 #pragma unroll
-    for (int i = 0; i < SP2_ROWS; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
+    for (int i = 0; i < R; ++i) rows[i] = i < nrows ? __ldg(sigma_o + (int64_t)t * V + r0 + i) : 0;
 #pragma unroll
     for (int rr = 0; rr < NS; ++rr) {
       if (rr >= nrows) break;
@@ -1602,7 +1603,7 @@ __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
       const IDX* src = sig_idx + (idx_stride ? (int64_t)t * idx_stride : (int64_t)b);
       bulk((uint32_t)__cvta_generic_to_shared(s_idx), src, ((uint32_t)k * (uint32_t)sizeof(IDX) + 15u) & ~15u, ibar);
 #pragma unroll
-      for (int rr = NS; rr < SP2_ROWS; ++rr) {
+      for (int rr = NS; rr < R; ++rr) {
         if (rr >= nrows) break;
         const int slot = rr % NS, use = rr / NS;
         sp_mbar_wait(empty0 + 8 * slot, (use - 1) & 1);
@@ -2184,10 +2185,16 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
 #endif
     const size_t s2 = (size_t)nslot * rowb + idx_bytes;
     const bool streamed = (p->n % 8) == 0 && p->n <= 65536 && (ldw % 8) == 0 && ((uintptr_t)W & 15) == 0 &&
-                          nslot >= 4 && p->V % SP2_ROWS == 0 && s2 <= 200 * 1024 &&
+                          nslot >= 4 && p->V % 16 == 0 && s2 <= 200 * 1024 &&
                           ((uintptr_t)p->a_vals & 31) == 0 && ((uintptr_t)si & 15) == 0;
     if (streamed) {
-      const dim3 grid(p->V / SP2_ROWS, p->T), block(32 * (SP2_CWARPS + 1));
+      // 32 rows per CTA when one CTA's ring and list take more than half the SM's shared memory
+      // (the 4096 x 11008 down projection: 0.139 -> 0.135 ms), else 16
+      int rows = s2 > 113 * 1024 && p->V % 32 == 0 ? 32 : 16;
+#ifdef HINM_EXPERIMENTS
+      if (getenv("HINM_SP2")) rows = 16;  // the timing-only variants are instantiated with 16 rows
+#endif
+      const dim3 grid(p->V / rows, p->T), block(32 * (SP2_CWARPS + 1));
       auto go = [&](auto kern, const auto* idx, int stride) -> int {
         HINM_CUDA_TRY(smem_optin((const void*)kern, (int)s2 + 4096));
         HINM_CUDA_TRY(launch_chain(kern, grid, block, s2, stream, W, ldw, sigma_o, sp, idx, stride, p->n, p->V,
@@ -2207,8 +2214,12 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
                          : (dbg == 1 ? go(k_select_pack2<1, 4, uint16_t>, s16, p->n) : go(k_select_pack2<2, 4, uint16_t>, s16, p->n));
       else
 #endif
-      if (idx16)
+      if (idx16 && rows == 32)
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t, 32>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t, 32>, s16, p->n);
+      else if (idx16)
         rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t>, s16, p->n);
+      else if (rows == 32)
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t, 32>, si, 0) : go(k_select_pack2<0, 4, int32_t, 32>, si, 0);
       else
         rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t>, si, 0) : go(k_select_pack2<0, 4, int32_t>, si, 0);
       if (rc2) return rc2;
