@@ -1532,8 +1532,7 @@ __device__ __forceinline__ int4 grp_idx(const uint16_t* s, int g) {
 }
 
 // sig_idx: tile t's ids at sig_idx + sig_ptr[t] (idx_stride == 0) or at sig_idx + t * idx_stride.
-// R = rows per CTA (16; 32 when a CTA's ring fills the SM: the per-CTA start-up is then paid once
-// per 32 rows instead of 16)
+// R = rows per CTA (8, or 32 when one CTA's ring fills the SM; see the launch)
 template <int DBG = 0, int NS = 8, typename IDX = int32_t, int R = 16>
 __global__ void __launch_bounds__(32 * (SP2_CWARPS + 1)) k_select_pack2(
     const uint16_t* __restrict__ W, int64_t ldw, const int32_t* __restrict__ sigma_o,
@@ -2188,11 +2187,13 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
                           nslot >= 4 && p->V % 16 == 0 && s2 <= 200 * 1024 &&
                           ((uintptr_t)p->a_vals & 31) == 0 && ((uintptr_t)si & 15) == 0;
     if (streamed) {
-      // 32 rows per CTA when one CTA's ring and list take more than half the SM's shared memory
-      // (the 4096 x 11008 down projection: 0.139 -> 0.135 ms), else 16
-      int rows = s2 > 113 * 1024 && p->V % 32 == 0 ? 32 : 16;
+      // rows per CTA: 32 when one CTA's ring and list take more than half the SM's shared memory (the
+      // 4096 x 11008 down projection, one CTA per SM: the start-up is paid once per 32 rows), else 8
+      // (several CTAs per SM: finer CTAs balance better; 8 / 16 / 32 rows measured, scripts/r03_gpu80.sh)
+      int rows = s2 > 113 * 1024 && p->V % 32 == 0 ? 32 : 8;
 #ifdef HINM_EXPERIMENTS
       if (getenv("HINM_SP2")) rows = 16;  // the timing-only variants are instantiated with 16 rows
+      if (const char* e = getenv("HINM_SP2_ROWS")) rows = atoi(e) == 16 ? 16 : atoi(e) == 32 ? 32 : 8;
 #endif
       const dim3 grid(p->V / rows, p->T), block(32 * (SP2_CWARPS + 1));
       auto go = [&](auto kern, const auto* idx, int stride) -> int {
@@ -2212,16 +2213,19 @@ extern "C" int hinm_compress_bf16(const uint16_t* W, int64_t ldw, const double* 
       if (dbg && idx16)
         rc2 = nslot == 8 ? (dbg == 1 ? go(k_select_pack2<1, 8, uint16_t>, s16, p->n) : go(k_select_pack2<2, 8, uint16_t>, s16, p->n))
                          : (dbg == 1 ? go(k_select_pack2<1, 4, uint16_t>, s16, p->n) : go(k_select_pack2<2, 4, uint16_t>, s16, p->n));
+      else if (rows == 16)
+        rc2 = idx16 ? (nslot == 8 ? go(k_select_pack2<0, 8, uint16_t, 16>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t, 16>, s16, p->n))
+                    : (nslot == 8 ? go(k_select_pack2<0, 8, int32_t, 16>, si, 0) : go(k_select_pack2<0, 4, int32_t, 16>, si, 0));
       else
 #endif
       if (idx16 && rows == 32)
         rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t, 32>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t, 32>, s16, p->n);
       else if (idx16)
-        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t>, s16, p->n);
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, uint16_t, 8>, s16, p->n) : go(k_select_pack2<0, 4, uint16_t, 8>, s16, p->n);
       else if (rows == 32)
         rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t, 32>, si, 0) : go(k_select_pack2<0, 4, int32_t, 32>, si, 0);
       else
-        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t>, si, 0) : go(k_select_pack2<0, 4, int32_t>, si, 0);
+        rc2 = nslot == 8 ? go(k_select_pack2<0, 8, int32_t, 8>, si, 0) : go(k_select_pack2<0, 4, int32_t, 8>, si, 0);
       if (rc2) return rc2;
     } else {
       // one CTA per (tile, 4 rows), weight rows double-buffered through shared memory
