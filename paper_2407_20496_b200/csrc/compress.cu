@@ -1982,10 +1982,15 @@ static int vector_prune_impl(const uint16_t* W, int64_t ldw, const double* Wd, i
       // ghist[0..BSEL_BINS) histogram, then the candidate count and list (zeroed with the histogram)
       unsigned int* ncand = (unsigned int*)(ghist + BSEL_BINS);
       unsigned long long* cand = (unsigned long long*)(ghist + BSEL_BINS + 4);
-      // few CTAs with several keys per thread: every CTA flushes its shared histogram with global
+      // half the SMs at most, >= 2048 keys per CTA: every CTA flushes its shared histogram with global
       // atomics and scans the global one, so 2 x SMs CTAs spent their time on those fixed costs
       unsigned long long* xsel = keybits + 2;
-      const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms / 4, ceil_div(total, 4096)));
+      int bdiv = 2, bkeys = 2048;  // SMs / 4 and 4096 keys per CTA: 1.5 % slower (scripts/r03_gpu82.sh)
+#ifdef HINM_EXPERIMENTS
+      if (const char* e = getenv("HINM_BSEL_DIV")) bdiv = std::max(1, atoi(e));
+      if (const char* e = getenv("HINM_BSEL_KEYS")) bkeys = std::max(256, atoi(e));
+#endif
+      const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sms / bdiv, ceil_div(total, bkeys)));
       HINM_CUDA_TRY(launch_chain(k_bsel_hist<1024>, nblk, 1024, 0, stream, gains, total, keybits, ghist));
       unsigned int* done = ncand + 1;  // two "last CTA" counters, zeroed with the histogram
       HINM_CUDA_TRY(launch_chain(k_bsel_collect<1024>, nblk, 1024, 0, stream, gains, total, T, G, groups, keybits,
