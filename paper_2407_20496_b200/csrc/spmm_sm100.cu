@@ -817,7 +817,14 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
         return p.out_order == HINM_ORDER_ORIGINAL ? (int64_t)__ldg(p.sigma_o + prow) : prow;
       };
       // 32 accumulator columns (fp32 bits) -> bf16 -> 4 x 16-byte stores of one row segment
+#if defined(HINM_Y_POLICY) && HINM_Y_POLICY == 1  // experiments: Y stores evict_normal / evict_last
+      uint64_t pol_y;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_y));
+#elif defined(HINM_Y_POLICY) && HINM_Y_POLICY == 2
+      const uint64_t pol_y = l2_policy_evict_last();
+#else
       const uint64_t pol_y = l2_policy_evict_first();
+#endif
       auto store32 = [&](uint16_t* yrow, int col, const uint32_t (&v)[32]) {
         if (p.y_align32 && col + 32 <= p.B) {  // 2 x 32-byte stores: one full sector each
 #pragma unroll
@@ -885,6 +892,10 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
           if (lane == 0) release(acc);
           continue;
         }
+        if (DBG == 13) {  // experiment: release at once, then the drain and the stores (stores off the critical path)
+          __syncwarp();
+          if (lane == 0) release(acc);
+        }
         uint32_t v0[32], v1[32];
         if (NCH == 1) {  // one chunk per warp (M=64, BNT=128)
           tmem_ld_16x32bx2_x32<true, BNT / 2>(t_acc, v0);
@@ -906,12 +917,12 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
             tmem_ld_32x32b_x32<false>(t_acc + c * 32 + 32, v1);
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (c + 2 == NCH) {
+          if (c + 2 == NCH && DBG != 13) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) release(acc);
           }
-          if (live) {
+          if (live && DBG != 12) {  // 12 (experiment): the drain without the stores
             store32(yrow, col_base + c * 32, v0);
             store32(yrow, col_base + c * 32 + 32, v1);
           }
@@ -1027,6 +1038,8 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
     if (e[0] == '9') kern = k_hinm_spmm<128, 8, 9, false, 128, true>;
     if (!strcmp(e, "10")) kern = k_hinm_spmm<128, 8, 10, false, 128, true>;
     if (!strcmp(e, "11")) kern = k_hinm_spmm<128, 8, 11, false, 128, true>;
+    if (!strcmp(e, "12")) kern = k_hinm_spmm<128, 8, 12, false, 128, true>;
+    if (!strcmp(e, "13")) kern = k_hinm_spmm<128, 8, 13, false, 128, true>;
   }
 #endif
   const SmemLayout L = smem_layout(128, KS, false, 128, true);
