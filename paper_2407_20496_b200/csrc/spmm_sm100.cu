@@ -862,7 +862,9 @@ __global__ void __launch_bounds__(32 * kernel_warps(GW, PAIR), 1)
         nxt = unit_params<PAIR>(p, u + ugrid, crank);
         if (u + ugrid < p.units) nxt_row = out_row(nxt);
         const bool live = orow >= 0;
-        uint16_t* yrow = p.Y + (live ? orow : 0) * p.ldy;
+        // 14 (experiment): the same stores folded into a 64-row window of Y (L2-resident: the LSU / L2
+        // traffic of the stores without their DRAM writes)
+        uint16_t* yrow = p.Y + (live ? (DBG == 14 ? orow % 64 : orow) : 0) * p.ldy;
         const int col_base = cur.nb * NTOK + c_own + h * NCH * 32;
         if (cur.kp == 0) {  // empty tile: zero rows (spmm.py:89-90)
           for (int c = 0; c < NCH * 4; ++c)
@@ -1040,6 +1042,7 @@ int spmm_pair(const hinm_pack_t* g, const uint16_t* X, int64_t ldx, int B, uint1
     if (!strcmp(e, "11")) kern = k_hinm_spmm<128, 8, 11, false, 128, true>;
     if (!strcmp(e, "12")) kern = k_hinm_spmm<128, 8, 12, false, 128, true>;
     if (!strcmp(e, "13")) kern = k_hinm_spmm<128, 8, 13, false, 128, true>;
+    if (!strcmp(e, "14")) kern = k_hinm_spmm<128, 8, 14, false, 128, true>;
   }
 #endif
   const SmemLayout L = smem_layout(128, KS, false, 128, true);
