@@ -277,6 +277,7 @@ def run_llama(args):
 
     # weights: rank 0 compresses, NCCL replicates the packs (outside the timed region)
     packs, dense, sos, comp, group_ms = {}, {}, {}, {}, {}
+    comp_conc = None
     for i, (name, m, n) in enumerate(layer_shapes()):
         g = torch.Generator(device=dev).manual_seed(1000 + i)
         dense[name] = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -303,6 +304,7 @@ def run_llama(args):
         gpu_ms = compress_gpu_ms(H, torch, dense, cfg, sos)
         for j, name in enumerate(names_of()):
             comp[name] = (t_wall[j], ev[j].elapsed_time(ev[j + 1]), gpu_ms.get(name))
+        comp_conc = gpu_ms.get("_layers_concurrent")
         # the union-group image (hinm_group_plan + hinm_group_build): a one-time weight transform
         # next to the compressor, timed on its own (host wall; it synchronizes twice)
         if args.v in (32, 64):
@@ -424,7 +426,8 @@ def run_llama(args):
     if d.rank == 0:
         result = llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value,
                             ms_cold, cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e,
-                            ms_link, xh, yh, chunk, launches, group_ms, per_kernel_image)
+                            ms_link, xh, yh, chunk, launches, group_ms, per_kernel_image,
+                            comp_conc=comp_conc)
     # secondary rows (rank 0, N=1 only): the same step at V=128; both arms sustained at the power cap
     if d.world == 1 and not args.no_extras and args.v == 64:
         result["v128"] = v128_row(H, torch, dev, X, y, args, cublas, global_tokens)
@@ -495,6 +498,31 @@ def compress_gpu_ms(H, torch, dense, cfg, sos, reps=5):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         out[name] = statistics.median(ts)
+    # the three layers in one call of compress_layers (one side stream each, forked from and joined
+    # into the capturing stream): the same packs, the latency-bound middle of one layer's chain
+    # overlapping another layer's passes over W
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    names = list(names_of())
+    try:
+        with torch.cuda.stream(s):
+            H.compress_layers([dense[k] for k in names], cfg, [sos[k] for k in names], groups=False)
+            with torch.cuda.graph(g, stream=s):
+                H.compress_layers([dense[k] for k in names], cfg, [sos[k] for k in names], groups=False)
+    except Exception:  # pragma: no cover - capture unsupported
+        return out
+    torch.cuda.current_stream().wait_stream(s)
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        a, b = _events(torch, 2)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    out["_layers_concurrent"] = statistics.median(ts)
     return out
 
 
@@ -515,7 +543,7 @@ def pair_floor(pack, tokens, sms=148):
 
 def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value, ms_cold,
                cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e, ms_link, xh, yh, chunk,
-               launches, group_ms, per_kernel_image):
+               launches, group_ms, per_kernel_image, comp_conc=None):
     pk, kind = peaks()
     p_sparse = 2.0 * pk["bf16_tflops"]
     f_sp = sparse_flops(tokens)
@@ -639,11 +667,16 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                        "hbm_frac_stream": round(comp_bytes / (comp_gpu * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
                        "hbm_frac_gpu": None if not comp_graph else
                        round(comp_bytes / (comp_graph * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                       "layers_concurrent_gpu_ms": None if not comp_conc else round(comp_conc, 4),
+                       "hbm_frac_layers_concurrent": None if not comp_conc else
+                       round(comp_bytes / (comp_conc * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
                        "union_group_image_ms": {k: round(v, 2) for k, v in group_ms.items()},
                        "note": "hinm_compress_bf16 (reference view + per-tile image), three layers back to back "
                                "after two warm-up passes: ms = host wall per call, stream_ms = CUDA events "
                                "between consecutive calls, gpu_ms = one call captured in a CUDA graph and "
-                               "replayed after an L2 flush; union_group_image_ms = hinm_group_plan + "
+                               "replayed after an L2 flush; layers_concurrent_gpu_ms = the three layers in one "
+                               "compress_layers call (a side stream each) captured and replayed the same way; "
+                               "union_group_image_ms = hinm_group_plan + "
                                "hinm_group_build (a one-time weight transform, host wall); rank 0"},
         "e2e": {"value": round(eff_flops(global_tokens) / (ms_e2e * 1e-3) / 1e12, 2),
                 "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 4),

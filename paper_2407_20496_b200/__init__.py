@@ -22,7 +22,8 @@ from .permutation import (Partition, PruneReport, ScheduleState, ablation_mode, 
                           balanced_kmeans, gyro_permute, hungarian, icp_tile, no_perm_prune,
                           ocp_iterate, retained_saliency, sample_channels)
 from . import io
-from .device import DevicePack, HostChain, build_group_image, build_operand_image, compress, spmm, spmm_simt
+from .device import (DevicePack, HostChain, build_group_image, build_operand_image, compress,
+                     compress_layers, spmm, spmm_simt)
 
 __version__ = "0.1.0"
 
@@ -37,7 +38,8 @@ __all__ = [
     "masked_dense_from_encoding", "nm_prune", "restore_row_order", "survivors_per_tile",
     "validate_masks", "vector_prune", "TileBuffer", "dense_matmul", "gather_tile_buffer",
     "hinm_spmm", "hinm_spmm_original_order", "relative_error", "DevicePack",
-    "build_operand_image", "build_group_image", "compress", "spmm", "spmm_simt", "HostChain", "LayerChain",
+    "build_operand_image", "build_group_image", "compress", "compress_layers", "spmm",
+    "spmm_simt", "HostChain", "LayerChain",
     "build_layer_chain", "compose_layers", "kept_triples", "shuffle_encoding",
     "tile_shuffle_check", "no_perm_prune", "io", "PruneReport", "ablation_mode",
     "balanced_kmeans", "gyro_permute", "hungarian", "icp_tile", "ocp_iterate",

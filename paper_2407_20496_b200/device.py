@@ -350,6 +350,64 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
     return pack
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_streams(dev, count: int):
+    """Cached side streams of ``dev`` for compress_layers (their workspaces stay cached too)."""
+    torch = _torch()
+    lst = _SIDE_STREAMS.setdefault(dev.index, [])
+    while len(lst) < count:
+        lst.append(torch.cuda.Stream(device=dev))
+    return lst[:count]
+
+
+def compress_layers(weights, cfg, sigma_o, groups: bool | None = None, streams: int = 3):
+    """Compress several independent weights at once: layer i runs ``compress`` on side stream
+    i % ``streams`` (forked from and joined back into the current stream), so the latency-bound
+    middle of one layer's chain (tile rank, budget select, survivors: few CTAs, dependent L2 round
+    trips) overlaps the HBM passes over another layer's W.  Same packs as one ``compress`` per
+    layer (the kernels and the per-stream workspaces are independent); the caller's stream sees
+    every pack complete.  ``cfg`` / ``sigma_o``: one per layer, or ``cfg`` shared.  The
+    union-group images (host-synchronising) are built afterwards on the current stream."""
+    torch = _torch()
+    weights = list(weights)
+    if not weights:
+        return []
+    cfgs = list(cfg) if isinstance(cfg, (list, tuple)) else [cfg] * len(weights)
+    sigmas = list(sigma_o)
+    if len(cfgs) != len(weights) or len(sigmas) != len(weights):
+        raise ShapeMismatch(f"{len(weights)} weights, {len(cfgs)} configs, {len(sigmas)} sigma_o")
+    for w in weights:
+        _require_cuda(w, "weights")
+    dev = weights[0].device
+    if any(w.device != dev for w in weights):
+        raise ValueError("compress_layers: all weights must be on one device")
+    cur = torch.cuda.current_stream(dev)
+    side = _side_streams(dev, max(1, min(streams, len(weights))))
+    for s in side:
+        s.wait_stream(cur)
+    packs = []
+    for i, (w, c, so) in enumerate(zip(weights, cfgs, sigmas)):
+        s = side[i % len(side)]
+        with torch.cuda.stream(s):
+            p = compress(w, c, so, groups=False)
+        # the pack's one allocation was made on s and is read on the caller's stream from now on
+        # (under graph capture it lives in the graph's pool until the graph is destroyed)
+        if not torch.cuda.is_current_stream_capturing():
+            p.sigma_o.record_stream(cur)
+        packs.append(p)
+    for s in side:
+        cur.wait_stream(s)
+    for p in packs:
+        g = groups
+        if g is None:
+            g = p.has_operand_image and group_supported(p) and p.m >= 256
+        if g:
+            build_group_image(p)
+    return packs
+
+
 def build_operand_image(pack: DevicePack) -> DevicePack:
     """(Re)build the tcgen05 operand image of a pack from its reference view."""
     torch = _torch()
