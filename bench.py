@@ -277,7 +277,7 @@ def run_llama(args):
 
     # weights: rank 0 compresses, NCCL replicates the packs (outside the timed region)
     packs, dense, sos, comp, group_ms = {}, {}, {}, {}, {}
-    comp_conc = None
+    comp_conc = comp_conc_stream = None
     for i, (name, m, n) in enumerate(layer_shapes()):
         g = torch.Generator(device=dev).manual_seed(1000 + i)
         dense[name] = torch.randn(m, n, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
@@ -305,6 +305,21 @@ def run_llama(args):
         for j, name in enumerate(names_of()):
             comp[name] = (t_wall[j], ev[j].elapsed_time(ev[j + 1]), gpu_ms.get(name))
         comp_conc = gpu_ms.get("_layers_concurrent")
+        # the same compress_layers call eager (the host enqueues the three chains on side streams):
+        # CUDA events on the caller's stream around the call, median of 5 after a warm-up call
+        lay = list(names_of())
+        H.compress_layers([dense[k] for k in lay], cfg, [sos[k] for k in lay], groups=False)
+        conc_s = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            a, b = _events(torch, 2)
+            a.record()
+            tmp = H.compress_layers([dense[k] for k in lay], cfg, [sos[k] for k in lay], groups=False)
+            b.record()
+            torch.cuda.synchronize()
+            conc_s.append(a.elapsed_time(b))
+            del tmp
+        comp_conc_stream = statistics.median(conc_s)
         # the union-group image (hinm_group_plan + hinm_group_build): a one-time weight transform
         # next to the compressor, timed on its own (host wall; it synchronizes twice)
         if args.v in (32, 64):
@@ -427,7 +442,7 @@ def run_llama(args):
         result = llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value,
                             ms_cold, cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e,
                             ms_link, xh, yh, chunk, launches, group_ms, per_kernel_image,
-                            comp_conc=comp_conc)
+                            comp_conc=comp_conc, comp_conc_stream=comp_conc_stream)
     # secondary rows (rank 0, N=1 only): the same step at V=128; both arms sustained at the power cap
     if d.world == 1 and not args.no_extras and args.v == 64:
         result["v128"] = v128_row(H, torch, dev, X, y, args, cublas, global_tokens)
@@ -543,7 +558,8 @@ def pair_floor(pack, tokens, sms=148):
 
 def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_step, value, ms_cold,
                cublas, ms_cublas_step, cublas_tflops, clk, clk_cublas, ms_e2e, ms_link, xh, yh, chunk,
-               launches, group_ms, per_kernel_image, comp_conc=None):
+               launches, group_ms, per_kernel_image, comp_conc=None,
+               comp_conc_stream=None):
     pk, kind = peaks()
     p_sparse = 2.0 * pk["bf16_tflops"]
     f_sp = sparse_flops(tokens)
@@ -670,12 +686,16 @@ def llama_line(args, d, global_tokens, tokens, packs, comp, per_kernel, pct, ms_
                        "layers_concurrent_gpu_ms": None if not comp_conc else round(comp_conc, 4),
                        "hbm_frac_layers_concurrent": None if not comp_conc else
                        round(comp_bytes / (comp_conc * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                       "layers_concurrent_stream_ms": None if not comp_conc_stream else round(comp_conc_stream, 4),
+                       "hbm_frac_layers_concurrent_stream": None if not comp_conc_stream else
+                       round(comp_bytes / (comp_conc_stream * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
                        "union_group_image_ms": {k: round(v, 2) for k, v in group_ms.items()},
                        "note": "hinm_compress_bf16 (reference view + per-tile image), three layers back to back "
                                "after two warm-up passes: ms = host wall per call, stream_ms = CUDA events "
                                "between consecutive calls, gpu_ms = one call captured in a CUDA graph and "
                                "replayed after an L2 flush; layers_concurrent_gpu_ms = the three layers in one "
-                               "compress_layers call (a side stream each) captured and replayed the same way; "
+                               "compress_layers call (a side stream each) captured and replayed the same way, "
+                               "layers_concurrent_stream_ms = that call eager (CUDA events around it); "
                                "union_group_image_ms = hinm_group_plan + "
                                "hinm_group_build (a one-time weight transform, host wall); rank 0"},
         "e2e": {"value": round(eff_flops(global_tokens) / (ms_e2e * 1e-3) / 1e12, 2),

@@ -8,6 +8,7 @@ path when the library or a CUDA device is unavailable.
 from __future__ import annotations
 
 import ctypes
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,6 +34,26 @@ def _stream_handle(device=None) -> int:
         idx = device.index if isinstance(device, torch.device) else device
         return raw(torch.cuda.current_device() if idx is None else int(idx))
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class _NullCtx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULL_CTX = _NullCtx()
+
+
+def _on_device(dev):
+    """torch.cuda.device(dev), skipped when dev is already current (the common case: the context
+    switch costs more host time than the launches it wraps)."""
+    torch = _torch()
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        return _NULL_CTX
+    return torch.cuda.device(dev)
 
 
 def _ptr(t) -> int | None:
@@ -87,9 +108,10 @@ class DevicePack:
 
     def __setattr__(self, name, value):
         # any field change invalidates the cached C view of the pack
-        object.__setattr__(self, name, value)
+        d = self.__dict__
+        d[name] = value
         if name != "_struct_cache":
-            object.__setattr__(self, "_struct_cache", None)
+            d["_struct_cache"] = None
 
     def struct(self) -> _lib.PackStruct:
         """The C-ABI view (hinm_pack_t) of this pack; cached until a field is reassigned."""
@@ -224,6 +246,22 @@ def _empty_pack(vcfg: ValidatedConfig, device) -> DevicePack:
         kept=torch.empty(max(L, 1), dtype=torch.bfloat16, device=device))
 
 
+@functools.lru_cache(maxsize=256)
+def _pack_capacity(m: int, n: int, V: int, K: int) -> tuple[int, int, int]:
+    """hinm_pack_capacity (kpad_cap, meta words, a_vals elements), per shape."""
+    kc, mc, ac = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load().hinm_pack_capacity(m, n, V, K, ctypes.byref(kc), ctypes.byref(mc),
+                                              ctypes.byref(ac)), "pack_capacity")
+    return kc.value, mc.value, ac.value
+
+
+@functools.lru_cache(maxsize=256)
+def _compress_workspace_bytes(m: int, n: int, V: int, M: int) -> int:
+    nbytes = ctypes.c_size_t()
+    _lib.check(_lib.load().hinm_compress_workspace(m, n, V, M, ctypes.byref(nbytes)), "compress_workspace")
+    return nbytes.value
+
+
 _WS_CACHE: dict = {}
 _WS_LOCK = __import__("threading").Lock()
 
@@ -238,7 +276,7 @@ def _workspace(dev, stream: int, nbytes: int):
         if ws is None or ws.numel() < nbytes:
             ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
         _WS_CACHE[key] = ws
-        while len(_WS_CACHE) > 4:
+        while len(_WS_CACHE) > 8:
             _WS_CACHE.pop(next(iter(_WS_CACHE)))
     return ws
 
@@ -246,16 +284,19 @@ def _workspace(dev, stream: int, nbytes: int):
 def _carve(dev, parts):
     """One device allocation for all of a pack's arrays (256-byte aligned views)."""
     torch = _torch()
-    offs, total = [], 0
+    offs, sizes, total = [], [], 0
     for _, dtype, count in parts:
+        size = max(count, 1) * dtype.itemsize
         offs.append(total)
-        total += -(-max(count, 1) * torch.empty(0, dtype=dtype).element_size() // 256) * 256
+        sizes.append(size)
+        total += -(-size // 256) * 256
     buf = torch.empty(total, dtype=torch.uint8, device=dev)
-    out = {}
-    for (name, dtype, count), o in zip(parts, offs):
-        size = max(count, 1) * torch.empty(0, dtype=dtype).element_size()
-        out[name] = buf[o:o + size].view(dtype)
-    return out
+    # one split into [part, padding, part, padding, ...] views (one call instead of a slice per part)
+    cuts = []
+    for o, size, nxt in zip(offs, sizes, offs[1:] + [total]):
+        cuts += [size, nxt - o - size]
+    views = buf.split(cuts)
+    return {name: views[2 * i].view(dtype) for i, (name, dtype, _) in enumerate(parts)}
 
 
 def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | None = None,
@@ -289,25 +330,23 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
              ("nm_pos", torch.uint8, L), ("kept", torch.bfloat16, L), ("vector_mask", torch.uint8, T * n)]
     kc = mc = 0
     if build_operand_image:
-        kc_, mc_, ac_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _lib.check(lib.hinm_pack_capacity(m, n, V, K, ctypes.byref(kc_), ctypes.byref(mc_),
-                                          ctypes.byref(ac_)), "pack_capacity")
-        kc, mc = kc_.value, mc_.value
+        kc, mc, ac = _pack_capacity(m, n, V, K)
         parts += [("tile_kofs", torch.int32, T + 1), ("tile_eofs", torch.int32, T + 1),
-                  ("gidx", torch.int32, kc), ("a_vals", torch.bfloat16, ac_.value), ("a_meta", torch.int32, mc)]
+                  ("gidx", torch.int32, kc), ("a_vals", torch.bfloat16, ac), ("a_meta", torch.int32, mc)]
     a = _carve(dev, parts)
     if hasattr(sigma_o, "is_cuda"):
         a["sigma_o"].copy_(sigma_o.reshape(-1))
     else:
         # pinned staging: a pageable copy would synchronize the stream (and the compressions before)
-        host = torch.from_numpy(np.ascontiguousarray(sigma_o, dtype=np.int32)).pin_memory()
+        # (the caching host allocator keeps the block until the copy has run)
+        host = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        host.numpy()[:] = np.asarray(sigma_o).reshape(-1)
         a["sigma_o"].copy_(host, non_blocking=True)
     vmask = a.pop("vector_mask")
     pack = DevicePack(m, n, V, N, M, K, vcfg.config, kpad_cap=kc, meta_cap=mc, **a)
-    ws_bytes = ctypes.c_size_t()
-    _lib.check(lib.hinm_compress_workspace(m, n, V, M, ctypes.byref(ws_bytes)), "compress_workspace")
+    ws_nbytes = _compress_workspace_bytes(m, n, V, M)
     stream = _stream_handle(dev)
-    ws = _workspace(dev, stream, ws_bytes.value)
+    ws = _workspace(dev, stream, ws_nbytes)
     S = None
     if saliency is not None:
         from .model import SaliencyMatrix, as_values
@@ -336,11 +375,11 @@ def compress(weights, cfg, sigma_o, sigma_i=None, build_operand_image: bool | No
             np.empty(0, np.int64)
         si = torch.as_tensor(flat.astype(np.int32)).to(dev)
     st = pack.struct()
-    with torch.cuda.device(dev):
+    with _on_device(dev):
         status = lib.hinm_compress_bf16(weights.data_ptr(), weights.stride(0), _ptr(S),
                                         0 if S is None else S.stride(0), pack.sigma_o.data_ptr(),
                                         _ptr(sp), _ptr(si), ctypes.byref(st), vmask.data_ptr(),
-                                        ws.data_ptr(), ws_bytes.value, stream)
+                                        ws.data_ptr(), ws_nbytes, stream)
     _lib.check(status, "compress")
     pack.vector_mask = vmask.view(vcfg.num_tiles, n)
     if groups is None:
