@@ -402,13 +402,17 @@ def _side_streams(dev, count: int):
 
 
 def compress_layers(weights, cfg, sigma_o, groups: bool | None = None, streams: int = 3):
-    """Compress several independent weights at once: layer i runs ``compress`` on side stream
+    """Compress several independent weights at once: layer i's chain runs on side stream
     i % ``streams`` (forked from and joined back into the current stream), so the latency-bound
     middle of one layer's chain (tile rank, budget select, survivors: few CTAs, dependent L2 round
     trips) overlaps the HBM passes over another layer's W.  Same packs as one ``compress`` per
     layer (the kernels and the per-stream workspaces are independent); the caller's stream sees
-    every pack complete.  ``cfg`` / ``sigma_o``: one per layer, or ``cfg`` shared.  The
-    union-group images (host-synchronising) are built afterwards on the current stream."""
+    every pack complete.  ``cfg`` / ``sigma_o``: one per layer, or ``cfg`` shared.
+
+    Host path: one device allocation for all the packs (each pack's arrays are views into it),
+    one pinned upload of every sigma_o, and the chains launched on the side streams' raw handles,
+    so the host enqueues three layers faster than the GPU runs them.  The union-group images
+    (host-synchronising) are built afterwards on the current stream."""
     torch = _torch()
     weights = list(weights)
     if not weights:
@@ -417,27 +421,75 @@ def compress_layers(weights, cfg, sigma_o, groups: bool | None = None, streams: 
     sigmas = list(sigma_o)
     if len(cfgs) != len(weights) or len(sigmas) != len(weights):
         raise ShapeMismatch(f"{len(weights)} weights, {len(cfgs)} configs, {len(sigmas)} sigma_o")
-    for w in weights:
-        _require_cuda(w, "weights")
+    from .pruning import check_sigma_o
+
     dev = weights[0].device
-    if any(w.device != dev for w in weights):
-        raise ValueError("compress_layers: all weights must be on one device")
-    cur = torch.cuda.current_stream(dev)
-    side = _side_streams(dev, max(1, min(streams, len(weights))))
-    for s in side:
-        s.wait_stream(cur)
-    packs = []
+    layers, parts, m_tot = [], [], 0
     for i, (w, c, so) in enumerate(zip(weights, cfgs, sigmas)):
-        s = side[i % len(side)]
-        with torch.cuda.stream(s):
-            p = compress(w, c, so, groups=False)
-        # the pack's one allocation was made on s and is read on the caller's stream from now on
-        # (under graph capture it lives in the graph's pool until the graph is destroyed)
-        if not torch.cuda.is_current_stream_capturing():
-            p.sigma_o.record_stream(cur)
-        packs.append(p)
+        _require_cuda(w, "weights")
+        if w.dtype != torch.bfloat16 or w.dim() != 2:
+            raise ValueError("weights must be 2-D bfloat16 CUDA tensors")
+        if w.device != dev:
+            raise ValueError("compress_layers: all weights must be on one device")
+        m, n = w.shape
+        vcfg = ensure_validated(c, (m, n))
+        check_sigma_o(so, m)
+        V, N, M, K, T = vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group, vcfg.total_keep, vcfg.num_tiles
+        img = spmm_supported(V, N, M)
+        kc = mc = 0
+        parts += [(f"{i}tile_ptr", torch.int32, T + 1), (f"{i}vec_idx", torch.int32, K),
+                  (f"{i}nm_pos", torch.uint8, V * K // M * N), (f"{i}kept", torch.bfloat16, V * K // M * N),
+                  (f"{i}vector_mask", torch.uint8, T * n)]
+        if img:
+            kc, mc, ac = _pack_capacity(m, n, V, K)
+            parts += [(f"{i}tile_kofs", torch.int32, T + 1), (f"{i}tile_eofs", torch.int32, T + 1),
+                      (f"{i}gidx", torch.int32, kc), (f"{i}a_vals", torch.bfloat16, ac),
+                      (f"{i}a_meta", torch.int32, mc)]
+        layers.append((w, vcfg, so, img, kc, mc, m_tot))
+        m_tot += m
+    parts.append(("sigma_all", torch.int32, m_tot))
+    a = _carve(dev, parts)
+    sig_all = a.pop("sigma_all")
+    host = torch.empty(m_tot, dtype=torch.int32, pin_memory=True)
+    hv = host.numpy()
+    for w, _, so, _, _, _, off in layers:
+        if not hasattr(so, "is_cuda"):
+            hv[off:off + w.shape[0]] = np.asarray(so).reshape(-1)
+    sig_all.copy_(host, non_blocking=True)  # the caching host allocator keeps the block until it ran
+    for w, _, so, _, _, _, off in layers:
+        if hasattr(so, "is_cuda"):
+            sig_all[off:off + w.shape[0]].copy_(so.reshape(-1))
+    cur = torch.cuda.current_stream(dev)
+    capturing = torch.cuda.is_current_stream_capturing()
+    side = _side_streams(dev, max(1, min(streams, len(weights))))
+    fork = torch.cuda.Event()
+    fork.record(cur)
     for s in side:
-        cur.wait_stream(s)
+        s.wait_event(fork)
+    lib = _lib.load()
+    packs = []
+    with _on_device(dev):
+        for i, (w, vcfg, so, img, kc, mc, off) in enumerate(layers):
+            m, n = w.shape
+            s = side[i % len(side)]
+            sh = s.cuda_stream
+            f = {k[len(str(i)):]: v for k, v in a.items() if k.startswith(str(i)) and not k[len(str(i))].isdigit()}
+            vmask = f.pop("vector_mask")
+            pack = DevicePack(m, n, vcfg.vector_size, vcfg.nm_keep, vcfg.nm_group, vcfg.total_keep, vcfg.config,
+                              sigma_o=sig_all[off:off + m], kpad_cap=kc, meta_cap=mc, **f)
+            nbytes = _compress_workspace_bytes(m, n, vcfg.vector_size, vcfg.nm_group)
+            ws = _workspace(dev, sh, nbytes)
+            if not capturing:
+                ws.record_stream(s)  # allocated on the caller's stream, used on s
+            status = lib.hinm_compress_bf16(w.data_ptr(), w.stride(0), None, 0, pack.sigma_o.data_ptr(), None, None,
+                                            ctypes.byref(pack.struct()), vmask.data_ptr(), ws.data_ptr(), nbytes, sh)
+            _lib.check(status, "compress")
+            pack.vector_mask = vmask.view(vcfg.num_tiles, n)
+            packs.append(pack)
+    for s in side:
+        ev = torch.cuda.Event()
+        ev.record(s)
+        cur.wait_event(ev)
     for p in packs:
         g = groups
         if g is None:

@@ -39,7 +39,9 @@ def test_compress_layers_equals_per_layer_compress(streams):
     Ws = [torch.as_tensor(synth.randn_bf16(s, 10 + i)).to("cuda", torch.bfloat16)
           for i, s in enumerate(shapes)]
     sos = [synth.random_sigma_o(s[0], 20 + i) for i, s in enumerate(shapes)]
-    packs = H.compress_layers(Ws, cfgs, sos, groups=False, streams=streams)
+    # one sigma_o as a CUDA tensor (copied on the device), the others from the host
+    sos_in = [torch.as_tensor(so).cuda() if i == 1 else so for i, so in enumerate(sos)]
+    packs = H.compress_layers(Ws, cfgs, sos_in, groups=False, streams=streams)
     for W, c, so, p in zip(Ws, cfgs, sos, packs):
         _same(p, H.compress(W, c, so, groups=False))
     # bit-exact against the oracle for the first layer
