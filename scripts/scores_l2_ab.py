@@ -4,7 +4,8 @@ through compress_layers (CUDA graphs, L2 flushed before each replay; bench.compr
 
     HINM_B200_LIB=scripts/libhinm_b200_exp.so [HINM_SCORES_STREAM=1] python scripts/scores_l2_ab.py
 
-Measured in round 2 (scripts/r04_gpu3.sh): no difference; the knob and the evict_normal variant
+Measured in round 2 (scripts/r04_gpu3.sh, and r04_gpu6.sh for the HINM_SCORES_PIPE / _NT64 variants):
+no difference; the knobs and the variants
 were removed from compress.cu afterwards.
 """
 import json
@@ -29,5 +30,12 @@ ref = {k: H.compress(dense[k], cfg, sos[k], groups=False) for k in dense}
 out = bench.compress_gpu_ms(H, torch, dense, cfg, sos, reps=9)
 again = {k: H.compress(dense[k], cfg, sos[k], groups=False) for k in dense}
 same = all(torch.equal(ref[k].kept, again[k].kept) and torch.equal(ref[k].vec_idx, again[k].vec_idx) for k in ref)
-print(json.dumps({"stream": bool(os.environ.get("HINM_SCORES_STREAM")), "same_packs": same,
+import hashlib  # noqa: E402
+
+digest = hashlib.sha256()
+for k in sorted(ref):
+    for f in ("tile_ptr", "vec_idx", "nm_pos", "kept", "a_vals"):
+        digest.update(getattr(ref[k], f).view(torch.uint8).cpu().numpy().tobytes())
+knobs = {k: v for k, v in os.environ.items() if k.startswith("HINM_SCORES")}
+print(json.dumps({"knobs": knobs, "same_packs": same, "digest": digest.hexdigest()[:16],
                   **{k: round(v, 4) for k, v in out.items()}}))
